@@ -1,0 +1,827 @@
+// Host side of the C-ABI (include/whale_splitfc.h): shard plan, workspace layout, tile
+// configuration, TMA descriptors and the launch sequence of the split-FC forward/backward.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/whale_splitfc.h"
+#include "gemm_sm100.cuh"
+#include "kernels_aux.cuh"
+
+using namespace whale;
+
+// ============================================================================ errors
+static thread_local std::string g_last_error;
+
+static whale_status_t fail(whale_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      return fail(WHALE_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                  __LINE__);                                                                   \
+  } while (0)
+
+extern "C" const char* whale_last_error(void) { return g_last_error.c_str(); }
+
+// ============================================================================ plan (A1)
+// Hamilton / largest-remainder apportionment in exact integer arithmetic
+// (SPEC.md:281).  Ties in the remainder go to the lower rank.
+extern "C" whale_status_t whale_splitfc_plan(int64_t num_classes, int32_t world_size, const uint32_t* capacity,
+                                             int64_t* shard_counts, int64_t* shard_offsets) {
+  if (world_size < 1 || world_size > kMaxRanks)
+    return fail(WHALE_ERR_INVALID_ARG, "world_size %d outside [1, %d]", world_size, kMaxRanks);
+  if (num_classes < 1) return fail(WHALE_ERR_INVALID_ARG, "num_classes must be >= 1");
+  if (!shard_counts || !shard_offsets) return fail(WHALE_ERR_INVALID_ARG, "NULL output array");
+  const int N = world_size;
+  __int128 wsum = 0;
+  for (int i = 0; i < N; ++i) {
+    const uint32_t w = capacity ? capacity[i] : 1u;
+    if (w == 0) return fail(WHALE_ERR_INVALID_ARG, "capacity[%d] == 0 (weights must be > 0)", i);
+    wsum += w;
+  }
+  if (num_classes < N) return fail(WHALE_ERR_UNSPLITTABLE, "C=%lld < world=%d", (long long)num_classes, N);
+  int64_t q[kMaxRanks];
+  __int128 rho[kMaxRanks];
+  int64_t assigned = 0;
+  for (int i = 0; i < N; ++i) {
+    const __int128 num = static_cast<__int128>(num_classes) * (capacity ? capacity[i] : 1u);
+    q[i] = static_cast<int64_t>(num / wsum);
+    rho[i] = num % wsum;
+    assigned += q[i];
+  }
+  int order[kMaxRanks];
+  for (int i = 0; i < N; ++i) order[i] = i;
+  std::stable_sort(order, order + N, [&](int a, int b) { return rho[a] > rho[b]; });  // ties: lower rank
+  for (int64_t k = 0; k < num_classes - assigned; ++k) q[order[k]] += 1;
+  for (int i = 0; i < N; ++i)
+    if (q[i] == 0) return fail(WHALE_ERR_UNSPLITTABLE, "shard %d would receive 0 classes", i);
+  int64_t off = 0;
+  for (int i = 0; i < N; ++i) {
+    shard_counts[i] = q[i];
+    shard_offsets[i] = off;
+    off += q[i];
+  }
+  return WHALE_OK;
+}
+
+// ============================================================================ configuration
+struct GemmCfg {
+  int BN = 0, m_blocks = 0, n_blocks = 0, splits = 1, num_kb = 0, kb_per_split = 0, num_tiles = 0;
+  int stages = 0, stage_bytes = 0, smem = 0, grid = 0;
+};
+
+struct Layout {
+  // local workspace offsets
+  size_t P, m_tile, s_tile, zy, lse, row_loss, stats_local, dxpart, xg_local, yg_local, counters, local_total;
+  // fp32 (kind::tf32) backward only: K-major transposed operands
+  size_t XT = 0, GT = 0, WT = 0;
+  int64_t ld_bt = 0;
+  // symmetric buffer offsets (per parity for the slabs)
+  size_t flags, xg[2], yg[2], stats[2], dxrecv[2], symm_total;
+};
+
+enum FlagKind { FLAG_GATHER = 0, FLAG_STATS = 1, FLAG_RS = 2 };
+enum CounterIdx { CNT_GATHER = 0, CNT_STATS = 1, CNT_RS = 2, CNT_ERR = 16 };
+
+struct Plan {
+  int rank = 0, world = 1, es = 2;
+  int64_t B = 0, Bt = 0, D = 0, C = 0, Cr = 0, o_r = 0, ldp = 0;
+  int sms = 148;
+  GemmCfg fwd, dw, dx;
+  Layout L;
+};
+
+static constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+static int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
+
+static void finish_cfg(GemmCfg& g, int sms) {
+  g.stage_bytes = kStageABytes + g.BN * kRowBytes;
+  g.stages = std::min(8, (kSmemLimit - 1024 - kEpiBytes - 256) / g.stage_bytes);
+  g.smem = gemm_smem_bytes(g.stages, g.stage_bytes);
+  g.num_tiles = g.m_blocks * g.n_blocks * g.splits;
+  g.grid = std::min(g.num_tiles, sms);
+}
+
+// Pick BN (multiple of `gran`, <= 256) minimising waves x per-tile cost.
+static GemmCfg choose_plain(int64_t M, int64_t N, int64_t K, int gran, int kbk, int sms) {
+  GemmCfg best;
+  double best_cost = 1e300;
+  const int64_t nmax = std::min<int64_t>(256, align_up(N, gran));
+  for (int BN = static_cast<int>(nmax / gran * gran); BN >= gran; BN -= gran) {
+    GemmCfg g;
+    g.BN = BN;
+    g.m_blocks = cdiv(M, kBM);
+    g.n_blocks = cdiv(N, BN);
+    g.num_kb = cdiv(K, kbk);
+    g.splits = 1;
+    g.kb_per_split = g.num_kb;
+    const int64_t tiles = static_cast<int64_t>(g.m_blocks) * g.n_blocks;
+    const double cost = static_cast<double>(cdiv(tiles, sms)) * (BN + 48);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best = g;
+    }
+  }
+  finish_cfg(best, sms);
+  return best;
+}
+
+// dX: M = B_tot, N = D, K = C_r.  Split K so that tiles fill the SMs; partial sums go to
+// an fp32 [S x B_tot x D] buffer that the reduce-scatter sums in a fixed order.
+static GemmCfg choose_splitk(int64_t M, int64_t N, int64_t K, int gran, int kbk, int sms) {
+  GemmCfg best;
+  double best_cost = 1e300;
+  const int64_t nmax = std::min<int64_t>(256, align_up(N, gran));
+  const int num_kb = cdiv(K, kbk);
+  for (int BN = static_cast<int>(nmax / gran * gran); BN >= gran; BN -= gran) {
+    const int mb = cdiv(M, kBM), nb = cdiv(N, BN);
+    const int64_t mn = static_cast<int64_t>(mb) * nb;
+    for (int S = 1; S <= std::min(num_kb, 64); ++S) {
+      const int kbps = cdiv(num_kb, S);
+      const int Sr = cdiv(num_kb, kbps);
+      if (Sr != S) continue;
+      const int64_t tiles = mn * S;
+      const double kblock_bytes = (128.0 + BN) * kRowBytes;
+      const double cost = static_cast<double>(cdiv(tiles, sms)) * kbps * kblock_bytes +
+                          static_cast<double>(S) * M * N * 8.0 / sms;
+      if (cost < best_cost * 0.999) {
+        best_cost = cost;
+        GemmCfg g;
+        g.BN = BN;
+        g.m_blocks = mb;
+        g.n_blocks = nb;
+        g.splits = S;
+        g.num_kb = num_kb;
+        g.kb_per_split = kbps;
+        best = g;
+      }
+    }
+  }
+  finish_cfg(best, sms);
+  return best;
+}
+
+static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) {
+  if (!d) return fail(WHALE_ERR_INVALID_ARG, "NULL descriptor");
+  if (d->world_size < 1 || d->world_size > kMaxRanks)
+    return fail(WHALE_ERR_UNSUPPORTED, "world_size %d outside [1, %d]", d->world_size, kMaxRanks);
+  if (d->rank < 0 || d->rank >= d->world_size) return fail(WHALE_ERR_INVALID_ARG, "rank out of range");
+  if (d->local_batch < 1 || d->feature_dim < 1 || d->num_classes < 1)
+    return fail(WHALE_ERR_INVALID_ARG, "B, D and C must be >= 1");
+  if (d->feature_dim % 8 != 0) return fail(WHALE_ERR_UNSUPPORTED, "feature_dim %% 8 != 0 (TMA 16-byte rows)");
+  if (d->x_dtype != WHALE_BF16 && d->x_dtype != WHALE_F32) return fail(WHALE_ERR_UNSUPPORTED, "x_dtype");
+  if (d->dw_dtype != WHALE_F32) return fail(WHALE_ERR_UNSUPPORTED, "dw_dtype must be WHALE_F32");
+  if (!d->shard_counts || !d->shard_offsets) return fail(WHALE_ERR_INVALID_ARG, "NULL shard plan");
+  int64_t off = 0;
+  for (int r = 0; r < d->world_size; ++r) {
+    if (d->shard_counts[r] < 1 || d->shard_offsets[r] != off)
+      return fail(WHALE_ERR_INVALID_ARG, "shard plan is not a partition of [0, C) at rank %d", r);
+    off += d->shard_counts[r];
+  }
+  if (off != d->num_classes) return fail(WHALE_ERR_INVALID_ARG, "shard counts do not sum to C");
+  p.rank = d->rank;
+  p.world = d->world_size;
+  p.es = d->x_dtype == WHALE_BF16 ? 2 : 4;
+  p.B = d->local_batch;
+  p.Bt = p.B * p.world;
+  p.D = d->feature_dim;
+  p.C = d->num_classes;
+  p.Cr = d->shard_counts[p.rank];
+  p.o_r = d->shard_offsets[p.rank];
+  if (p.Bt > 65535) return fail(WHALE_ERR_UNSUPPORTED, "global batch > 65535");
+  if (p.Cr > (1ll << 31) - 256 || p.D > (1ll << 31) - 256) return fail(WHALE_ERR_UNSUPPORTED, "dimension too large");
+  const int vec = 16 / p.es;
+  p.ldp = static_cast<int64_t>(align_up(p.Cr, vec));
+  p.sms = sms;
+  const int kbk = kRowBytes / p.es;   // K elements per stage
+  const int atom = kRowBytes / p.es;  // MN-major atom / fwd P~ chunk
+  p.fwd = choose_plain(p.Bt, p.Cr, p.D, atom, kbk, sms);
+  p.dw = choose_plain(p.Cr, p.D, p.Bt, atom, kbk, sms);
+  p.dx = choose_splitk(p.Bt, p.D, p.Cr, atom, kbk, sms);
+
+  Layout& L = p.L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes, 1024);
+    return at;
+  };
+  const int T = p.fwd.n_blocks;
+  L.P = take(static_cast<size_t>(p.Bt) * p.ldp * p.es);
+  L.m_tile = take(static_cast<size_t>(p.Bt) * T * 4);
+  L.s_tile = take(static_cast<size_t>(p.Bt) * T * 4);
+  L.zy = take(p.Bt * 4);
+  L.lse = take(p.Bt * 4);
+  L.row_loss = take(p.Bt * 4);
+  L.stats_local = take(p.Bt * 16);
+  L.dxpart = take(static_cast<size_t>(p.dx.splits) * p.Bt * p.D * 4);
+  L.xg_local = take(p.world == 1 ? static_cast<size_t>(p.Bt) * p.D * p.es : 0);
+  L.yg_local = take(p.world == 1 ? p.Bt * 4 : 0);
+  L.counters = take(64 * 4);
+  if (p.es == 4) {
+    L.ld_bt = static_cast<int64_t>(align_up(p.Bt, 4));
+    L.XT = take(static_cast<size_t>(p.D) * L.ld_bt * 4);
+    L.GT = take(static_cast<size_t>(p.Cr) * L.ld_bt * 4);
+    L.WT = take(static_cast<size_t>(p.D) * p.ldp * 4);
+  }
+  L.local_total = o;
+  o = 0;
+  if (p.world > 1) {
+    L.flags = take(4 * kMaxRanks * 4);
+    for (int par = 0; par < 2; ++par) {
+      L.xg[par] = take(static_cast<size_t>(p.Bt) * p.D * p.es);
+      L.yg[par] = take(p.Bt * 4);
+      L.stats[par] = take(static_cast<size_t>(p.world) * p.Bt * 16);
+      L.dxrecv[par] = take(static_cast<size_t>(p.world) * p.B * p.D * 4);
+    }
+  }
+  L.symm_total = o;
+  return WHALE_OK;
+}
+
+extern "C" whale_status_t whale_splitfc_workspace_size(const whale_splitfc_desc* desc, size_t* symm_bytes,
+                                                       size_t* local_bytes) {
+  Plan p;
+  // SM count only shapes the tile choice; query it if a device is present, else 148.
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0) sms = v;
+  } else {
+    cudaGetLastError();
+  }
+  whale_status_t st = build_plan(desc, p, sms);
+  if (st != WHALE_OK) return st;
+  if (symm_bytes) *symm_bytes = p.L.symm_total;
+  if (local_bytes) *local_bytes = p.L.local_total;
+  return WHALE_OK;
+}
+
+// ============================================================================ TMA descriptors
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static whale_status_t get_encoder() {
+  if (g_encode) return WHALE_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(WHALE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return WHALE_OK;
+}
+
+// rank-2 or rank-3 map; dims/box innermost first; strides in bytes for dims 1..rank-1.
+static whale_status_t make_map(CUtensorMap* m, const void* base, int es, int rank, const uint64_t* dims,
+                               const uint64_t* strides, const uint32_t* box) {
+  whale_status_t st = get_encoder();
+  if (st != WHALE_OK) return st;
+  if (reinterpret_cast<uintptr_t>(base) % 16 != 0) return fail(WHALE_ERR_INVALID_ARG, "tensor base not 16-byte aligned");
+  cuuint64_t gd[3], gs[2];
+  cuuint32_t bd[3], es1[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bd[i] = box[i];
+  }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides[i];
+  const CUtensorMapDataType dt = es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUresult r = g_encode(m, dt, rank, const_cast<void*>(base), gd, gs, bd, es1, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(WHALE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return WHALE_OK;
+}
+
+static whale_status_t map2d(CUtensorMap* m, const void* base, int es, uint64_t inner, uint64_t outer,
+                            uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  const uint64_t dims[2] = {inner, outer};
+  const uint64_t strides[1] = {row_bytes};
+  const uint32_t box[2] = {box_inner, box_outer};
+  return make_map(m, base, es, 2, dims, strides, box);
+}
+
+static whale_status_t map3d_f32(CUtensorMap* m, const void* base, uint64_t n, uint64_t rows, uint64_t splits) {
+  const uint64_t dims[3] = {n, rows, splits};
+  const uint64_t strides[2] = {n * 4, n * rows * 4};
+  const uint32_t box[3] = {32, 32, 1};
+  return make_map(m, base, 4, 3, dims, strides, box);
+}
+
+// ============================================================================ context
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+static const char* kKindNames[] = {"bridge_gather", "logits_gemm", "stats_combine", "softmax_grad",
+                                   "dw_gemm",       "dx_gemm",     "dx_rs_push",    "dx_rs_reduce"};
+enum KernelKind { K_GATHER, K_LOGITS, K_STATS, K_GRAD, K_DW, K_DX, K_RS_PUSH, K_RS_REDUCE, K_NUM };
+
+struct whale_splitfc_ctx {
+  Plan p;
+  uint8_t* ws = nullptr;
+  uint8_t* symm[kMaxRanks] = {};
+  // static maps
+  CUtensorMap tmX_fwd[2], tmX_dw[2], tmP_store, tmG_dx, tmG_dw, tmDxPart;
+  CUtensorMap tmGT, tmXT, tmWT;  // fp32 path: K-major transposed operands
+  // pointer-cached maps
+  const void* w_cached = nullptr;
+  CUtensorMap tmW_fwd, tmW_dx;
+  const void* dw_cached = nullptr;
+  CUtensorMap tmDW;
+  uint32_t epoch = 0;
+  bool have_fwd = false;
+  bool profile = false;
+  std::vector<ProfRec> prof;
+  double prof_ms[K_NUM] = {};
+  int64_t prof_n[K_NUM] = {};
+};
+
+template <typename T>
+static T* wsp(whale_splitfc_ctx* c, size_t off) {
+  return reinterpret_cast<T*>(c->ws + off);
+}
+
+static bool g_attr_done[8] = {};
+
+template <int EPI, bool AMN, bool BMN, int ES>
+static whale_status_t launch_gemm(whale_splitfc_ctx* c, int slot, const GemmCfg& g, const CUtensorMap& A,
+                                  const CUtensorMap& B, const CUtensorMap& O, const GemmArgs& args,
+                                  cudaStream_t s) {
+  auto kern = splitfc_gemm_kernel<EPI, AMN, BMN, ES>;
+  if (!g_attr_done[slot]) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+    g_attr_done[slot] = true;
+  }
+  kern<<<g.grid, kGemmThreads, g.smem, s>>>(A, B, O, args);
+  CUDA_TRY(cudaGetLastError());
+  return WHALE_OK;
+}
+
+static void prof_begin(whale_splitfc_ctx* c, int kind, cudaStream_t s, ProfRec& r) {
+  if (!c->profile) return;
+  r.kind = kind;
+  cudaEventCreate(&r.a);
+  cudaEventCreate(&r.b);
+  cudaEventRecord(r.a, s);
+}
+static void prof_end(whale_splitfc_ctx* c, cudaStream_t s, ProfRec& r) {
+  if (!c->profile) return;
+  cudaEventRecord(r.b, s);
+  c->prof.push_back(r);
+}
+
+#define PROFILED(kind, stream, body)            \
+  do {                                          \
+    ProfRec _r{};                               \
+    prof_begin(c, kind, stream, _r);            \
+    whale_status_t _st = (body);                \
+    if (_st != WHALE_OK) return _st;            \
+    prof_end(c, stream, _r);                    \
+  } while (0)
+
+static GemmArgs base_args(const GemmCfg& g, int M, int N) {
+  GemmArgs a{};
+  a.M = M;
+  a.N = N;
+  a.BN = g.BN;
+  a.m_blocks = g.m_blocks;
+  a.n_blocks = g.n_blocks;
+  a.splits = g.splits;
+  a.num_kb = g.num_kb;
+  a.kb_per_split = g.kb_per_split;
+  a.num_tiles = g.num_tiles;
+  a.stages = g.stages;
+  a.stage_bytes = g.stage_bytes;
+  return a;
+}
+
+extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, whale_splitfc_ctx** out) {
+  if (!out) return fail(WHALE_ERR_INVALID_ARG, "NULL out");
+  *out = nullptr;
+  int dev = 0, major = 0, sms = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (major != 10) return fail(WHALE_ERR_UNSUPPORTED, "needs an sm_100 (B200) device, found major %d", major);
+  auto* c = new whale_splitfc_ctx();
+  whale_status_t st = build_plan(desc, c->p, sms);
+  if (st != WHALE_OK) {
+    delete c;
+    return st;
+  }
+  const Plan& p = c->p;
+  if (!desc->local_workspace || desc->local_workspace_bytes < p.L.local_total ||
+      reinterpret_cast<uintptr_t>(desc->local_workspace) % 256) {
+    delete c;
+    return fail(WHALE_ERR_STATE, "local workspace missing, misaligned or < %zu bytes", p.L.local_total);
+  }
+  c->ws = static_cast<uint8_t*>(desc->local_workspace);
+  if (p.world > 1) {
+    if (!desc->peer_symm_ptrs || desc->symm_bytes < p.L.symm_total) {
+      delete c;
+      return fail(WHALE_ERR_STATE, "symmetric buffers missing or < %zu bytes", p.L.symm_total);
+    }
+    for (int r = 0; r < p.world; ++r) c->symm[r] = static_cast<uint8_t*>(desc->peer_symm_ptrs[r]);
+  }
+  // static TMA maps
+  const int es = p.es, kbk = kRowBytes / es, atom = kRowBytes / es;
+  for (int par = 0; par < 2; ++par) {
+    const void* xg = p.world == 1 ? static_cast<const void*>(c->ws + p.L.xg_local)
+                                  : static_cast<const void*>(c->symm[p.rank] + p.L.xg[par]);
+#define MAP_TRY(x)                 \
+  do {                             \
+    whale_status_t _s = (x);       \
+    if (_s != WHALE_OK) {          \
+      delete c;                    \
+      return _s;                   \
+    }                              \
+  } while (0)
+    MAP_TRY(map2d(&c->tmX_fwd[par], xg, es, p.D, p.Bt, p.D * es, kbk, kBM));
+    MAP_TRY(map2d(&c->tmX_dw[par], xg, es, p.D, p.Bt, p.D * es, atom, kbk));
+  }
+  void* P = c->ws + p.L.P;
+  MAP_TRY(map2d(&c->tmP_store, P, es, p.Cr, p.Bt, p.ldp * es, kRowBytes / es, 32));
+  MAP_TRY(map2d(&c->tmG_dx, P, es, p.Cr, p.Bt, p.ldp * es, kbk, kBM));
+  MAP_TRY(map2d(&c->tmG_dw, P, es, p.Cr, p.Bt, p.ldp * es, atom, kbk));
+  MAP_TRY(map3d_f32(&c->tmDxPart, c->ws + p.L.dxpart, p.D, p.Bt, p.dx.splits));
+  if (es == 4) {
+    const int64_t ldb = p.L.ld_bt;
+    MAP_TRY(map2d(&c->tmGT, c->ws + p.L.GT, 4, p.Bt, p.Cr, ldb * 4, kbk, kBM));
+    MAP_TRY(map2d(&c->tmXT, c->ws + p.L.XT, 4, p.Bt, p.D, ldb * 4, kbk, p.dw.BN));
+    MAP_TRY(map2d(&c->tmWT, c->ws + p.L.WT, 4, p.Cr, p.D, p.ldp * 4, kbk, p.dx.BN));
+  }
+#undef MAP_TRY
+  CUDA_TRY(cudaMemset(c->ws + p.L.counters, 0, 64 * 4));
+  *out = c;
+  return WHALE_OK;
+}
+
+extern "C" whale_status_t whale_splitfc_destroy(whale_splitfc_ctx* ctx) {
+  if (!ctx) return WHALE_OK;
+  for (auto& r : ctx->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  delete ctx;
+  return WHALE_OK;
+}
+
+// ============================================================================ forward
+// (re)encode the weight maps when the shard pointer changes (host-only, ~us)
+static whale_status_t ensure_w_maps(whale_splitfc_ctx* c, const void* w) {
+  if (w == c->w_cached) return WHALE_OK;
+  const Plan& p = c->p;
+  const int kbk = kRowBytes / p.es, atom = kRowBytes / p.es;
+  whale_status_t st = map2d(&c->tmW_fwd, w, p.es, p.D, p.Cr, p.D * p.es, kbk, p.fwd.BN);
+  if (st != WHALE_OK) return st;
+  st = map2d(&c->tmW_dx, w, p.es, p.D, p.Cr, p.D * p.es, atom, kbk);
+  if (st != WHALE_OK) return st;
+  c->w_cached = w;
+  return WHALE_OK;
+}
+
+template <int ES>
+static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, const int32_t* y_local,
+                                   const void* w, float* loss, float* row_loss, cudaStream_t s) {
+  const Plan& p = c->p;
+  const Layout& L = p.L;
+  const int par = c->epoch & 1;
+  unsigned* counters = wsp<unsigned>(c, L.counters);
+  int* err = reinterpret_cast<int*>(counters + CNT_ERR);
+
+  {
+    whale_status_t st = ensure_w_maps(c, w);
+    if (st != WHALE_OK) return st;
+  }
+  // ---- A2 bridge all-gather
+  PeerPtrs dx{}, dy{};
+  PeerFlags fl{};
+  void* xg_local_ptr;
+  int32_t* yg_local_ptr;
+  if (p.world == 1) {
+    dx.p[0] = c->ws + L.xg_local;
+    dy.p[0] = c->ws + L.yg_local;
+    xg_local_ptr = dx.p[0];
+    yg_local_ptr = static_cast<int32_t*>(dy.p[0]);
+  } else {
+    for (int r = 0; r < p.world; ++r) {
+      dx.p[r] = c->symm[r] + L.xg[par];
+      dy.p[r] = c->symm[r] + L.yg[par];
+      fl.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_GATHER * kMaxRanks + p.rank;
+    }
+    xg_local_ptr = c->symm[p.rank] + L.xg[par];
+    yg_local_ptr = reinterpret_cast<int32_t*>(c->symm[p.rank] + L.yg[par]);
+  }
+  (void)xg_local_ptr;
+  {
+    const int64_t x_vecs = p.B * p.D * ES / 16;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(x_vecs, 256), 2 * p.sms)));
+    PROFILED(K_GATHER, s, ([&]() -> whale_status_t {
+               bridge_gather_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(x_local), y_local, x_vecs,
+                                                         static_cast<int>(p.B), p.rank, p.world, dx, dy, fl,
+                                                         c->epoch, counters + CNT_GATHER);
+               CUDA_TRY(cudaGetLastError());
+               return WHALE_OK;
+             }()));
+  }
+  // ---- A3 logits GEMM with fused row statistics
+  {
+    GemmArgs a = base_args(p.fwd, static_cast<int>(p.Bt), static_cast<int>(p.Cr));
+    a.labels = yg_local_ptr;
+    a.class_offset = p.o_r;
+    a.m_tile = wsp<float>(c, L.m_tile);
+    a.s_tile = wsp<float>(c, L.s_tile);
+    a.zy = wsp<float>(c, L.zy);
+    a.err = err;
+    if (p.world > 1) {
+      a.wait_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_GATHER * kMaxRanks;
+      a.wait_count = p.world;
+      a.wait_epoch = c->epoch;
+    }
+    PROFILED(K_LOGITS, s,
+             (launch_gemm<EPI_FWD_STATS, false, false, ES>(c, ES == 2 ? 0 : 3, p.fwd, c->tmX_fwd[par],
+                                                           c->tmW_fwd, c->tmP_store, a, s)));
+  }
+  // ---- A4 + A5 statistics exchange, combine, loss
+  {
+    StatsArgs a{};
+    a.m_tile = wsp<float>(c, L.m_tile);
+    a.s_tile = wsp<float>(c, L.s_tile);
+    a.zy_r = wsp<float>(c, L.zy);
+    a.y = yg_local_ptr;
+    a.T = p.fwd.n_blocks;
+    a.Bt = static_cast<int>(p.Bt);
+    a.B = static_cast<int>(p.B);
+    a.rank = p.rank;
+    a.world = p.world;
+    a.o_r = p.o_r;
+    a.C_r = p.Cr;
+    a.C = p.C;
+    if (p.world == 1) {
+      a.my_stats = wsp<float4>(c, L.stats_local);
+    } else {
+      for (int r = 0; r < p.world; ++r) {
+        a.peer_stats.p[r] = c->symm[r] + L.stats[par];
+        a.peer_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_STATS * kMaxRanks + p.rank;
+      }
+      a.my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_STATS * kMaxRanks;
+      a.my_stats = reinterpret_cast<float4*>(c->symm[p.rank] + L.stats[par]);
+    }
+    a.epoch = c->epoch;
+    a.lse = wsp<float>(c, L.lse);
+    a.row_loss_all = wsp<float>(c, L.row_loss);
+    a.loss = loss;
+    a.row_loss_local = row_loss;
+    a.counter = counters + CNT_STATS;
+    a.err = err;
+    const int grid = std::max(1, std::min<int>(cdiv(p.Bt, 8), p.sms));
+    PROFILED(K_STATS, s, ([&]() -> whale_status_t {
+               stats_combine_kernel<<<grid, 256, 0, s>>>(a);
+               CUDA_TRY(cudaGetLastError());
+               return WHALE_OK;
+             }()));
+  }
+  return WHALE_OK;
+}
+
+extern "C" whale_status_t whale_splitfc_forward(whale_splitfc_ctx* ctx, const void* x_local,
+                                                const int32_t* labels_local, const void* w_shard, float* loss,
+                                                float* row_loss, void* stream) {
+  if (!ctx || !x_local || !labels_local || !w_shard || !loss) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
+  if (reinterpret_cast<uintptr_t>(x_local) % 16 || reinterpret_cast<uintptr_t>(w_shard) % 16)
+    return fail(WHALE_ERR_INVALID_ARG, "x_local / w_shard must be 16-byte aligned");
+  ctx->epoch += 1;
+  auto s = static_cast<cudaStream_t>(stream);
+  whale_status_t st = ctx->p.es == 2 ? forward_impl<2>(ctx, x_local, labels_local, w_shard, loss, row_loss, s)
+                                     : forward_impl<4>(ctx, x_local, labels_local, w_shard, loss, row_loss, s);
+  if (st == WHALE_OK) ctx->have_fwd = true;
+  return st;
+}
+
+// ============================================================================ backward
+template <int ES>
+static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* dx_local, void* dw,
+                                    cudaStream_t s) {
+  const Plan& p = c->p;
+  const Layout& L = p.L;
+  const int par = c->epoch & 1;
+  unsigned* counters = wsp<unsigned>(c, L.counters);
+  int* err = reinterpret_cast<int*>(counters + CNT_ERR);
+  const int32_t* yg = p.world == 1 ? wsp<int32_t>(c, L.yg_local)
+                                   : reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg[par]);
+  {
+    whale_status_t st = ensure_w_maps(c, w);
+    if (st != WHALE_OK) return st;
+  }
+  if (dw != c->dw_cached) {
+    whale_status_t st = map3d_f32(&c->tmDW, dw, p.D, p.Cr, 1);
+    if (st != WHALE_OK) return st;
+    c->dw_cached = dw;
+  }
+  // ---- A6 G = (softmax - onehot) / B_tot, in place over P~
+  {
+    constexpr int V = 16 / ES;
+    dim3 grid(cdiv(cdiv(p.Cr, V), 256), static_cast<unsigned>(p.Bt));
+    PROFILED(K_GRAD, s, ([&]() -> whale_status_t {
+               softmax_grad_kernel<ES><<<grid, 256, 0, s>>>(c->ws + L.P, p.ldp, static_cast<int>(p.Bt), p.Cr,
+                                                            p.fwd.BN, p.fwd.n_blocks, wsp<float>(c, L.m_tile),
+                                                            wsp<float>(c, L.lse), yg, p.o_r,
+                                                            static_cast<float>(1.0 / static_cast<double>(p.Bt)));
+               CUDA_TRY(cudaGetLastError());
+               return WHALE_OK;
+             }()));
+  }
+  if constexpr (ES == 2) {
+    // ---- A7 dW_r = G_r^T X  (A = G^T MN-major, B = X MN-major)
+    {
+      GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
+      a.err = err;
+      PROFILED(K_DW, s,
+               (launch_gemm<EPI_STORE_F32, true, true, 2>(c, 1, p.dw, c->tmG_dw, c->tmX_dw[par], c->tmDW, a, s)));
+    }
+    // ---- A8 dX partials = G_r W_r  (A = G K-major, B = W_r MN-major), split-K
+    {
+      GemmArgs a = base_args(p.dx, static_cast<int>(p.Bt), static_cast<int>(p.D));
+      a.err = err;
+      PROFILED(K_DX, s,
+               (launch_gemm<EPI_STORE_F32, false, true, 2>(c, 2, p.dx, c->tmG_dx, c->tmW_dx, c->tmDxPart, a, s)));
+    }
+  } else {
+    // kind::tf32 accepts K-major operands only (plain 128B swizzle): transpose G, X, W_r.
+    const void* xg = p.world == 1 ? static_cast<const void*>(c->ws + L.xg_local)
+                                  : static_cast<const void*>(c->symm[p.rank] + L.xg[par]);
+    auto tr = [&](const void* src, long long sld, void* dst, long long dld, int64_t R, int64_t Cc) -> whale_status_t {
+      dim3 grid(cdiv(Cc, 32), cdiv(R, 32));
+      transpose_f32_kernel<<<grid, dim3(32, 32), 0, s>>>(static_cast<const float*>(src), sld,
+                                                         static_cast<float*>(dst), dld, static_cast<int>(R),
+                                                         static_cast<int>(Cc));
+      CUDA_TRY(cudaGetLastError());
+      return WHALE_OK;
+    };
+    PROFILED(K_GRAD, s, (tr(c->ws + L.P, p.ldp, c->ws + L.GT, L.ld_bt, p.Bt, p.Cr)));
+    PROFILED(K_GRAD, s, (tr(xg, p.D, c->ws + L.XT, L.ld_bt, p.Bt, p.D)));
+    PROFILED(K_GRAD, s, (tr(w, p.D, c->ws + L.WT, p.ldp, p.Cr, p.D)));
+    {
+      GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
+      a.err = err;
+      PROFILED(K_DW, s, (launch_gemm<EPI_STORE_F32, false, false, 4>(c, 4, p.dw, c->tmGT, c->tmXT, c->tmDW, a, s)));
+    }
+    {
+      GemmArgs a = base_args(p.dx, static_cast<int>(p.Bt), static_cast<int>(p.D));
+      a.err = err;
+      PROFILED(K_DX, s,
+               (launch_gemm<EPI_STORE_F32, false, false, 4>(c, 5, p.dx, c->tmG_dx, c->tmWT, c->tmDxPart, a, s)));
+    }
+  }
+  // ---- A8 reduce-scatter to the DP owners
+  {
+    PeerPtrs recv{};
+    PeerFlags fl{};
+    if (p.world > 1) {
+      for (int r = 0; r < p.world; ++r) {
+        recv.p[r] = c->symm[r] + L.dxrecv[par];
+        fl.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_RS * kMaxRanks + p.rank;
+      }
+    }
+    const int64_t total = p.Bt * p.D / 4;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 2 * p.sms)));
+    PROFILED(K_RS_PUSH, s, ([&]() -> whale_status_t {
+               dx_push_kernel<ES><<<grid, 256, 0, s>>>(wsp<const float4>(c, L.dxpart), p.dx.splits,
+                                                       static_cast<int>(p.Bt), static_cast<int>(p.B),
+                                                       static_cast<int>(p.D), p.rank, p.world, recv, fl, c->epoch,
+                                                       dx_local, counters + CNT_RS);
+               CUDA_TRY(cudaGetLastError());
+               return WHALE_OK;
+             }()));
+    if (p.world > 1) {
+      const int64_t own = p.B * p.D / 4;
+      const int g2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(own, 256), 2 * p.sms)));
+      const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_RS * kMaxRanks;
+      PROFILED(K_RS_REDUCE, s, ([&]() -> whale_status_t {
+                 dx_reduce_kernel<ES><<<g2, 256, 0, s>>>(reinterpret_cast<const float4*>(recv.p[p.rank]),
+                                                         static_cast<int>(p.B), static_cast<int>(p.D), p.world,
+                                                         my_flags, c->epoch, dx_local, err);
+                 CUDA_TRY(cudaGetLastError());
+                 return WHALE_OK;
+               }()));
+    }
+  }
+  return WHALE_OK;
+}
+
+extern "C" whale_status_t whale_splitfc_backward(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
+                                                 void* dw_shard, void* stream) {
+  if (!ctx || !w_shard || !dx_local || !dw_shard) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
+  if (!ctx->have_fwd) return fail(WHALE_ERR_STATE, "backward called before forward");
+  if (reinterpret_cast<uintptr_t>(dx_local) % 16 || reinterpret_cast<uintptr_t>(dw_shard) % 16)
+    return fail(WHALE_ERR_INVALID_ARG, "dx_local / dw_shard must be 16-byte aligned");
+  auto s = static_cast<cudaStream_t>(stream);
+  whale_status_t st = ctx->p.es == 2 ? backward_impl<2>(ctx, w_shard, dx_local, dw_shard, s)
+                                     : backward_impl<4>(ctx, w_shard, dx_local, dw_shard, s);
+  if (st == WHALE_OK) ctx->have_fwd = false;
+  return st;
+}
+
+extern "C" whale_status_t whale_splitfc_check(whale_splitfc_ctx* ctx, void* stream) {
+  if (!ctx) return fail(WHALE_ERR_INVALID_ARG, "NULL ctx");
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  int* err = reinterpret_cast<int*>(wsp<unsigned>(ctx, ctx->p.L.counters) + CNT_ERR);
+  int h = 0;
+  CUDA_TRY(cudaMemcpy(&h, err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) CUDA_TRY(cudaMemset(err, 0, sizeof(int)));
+  if (h & ERR_LABEL) return fail(WHALE_ERR_LABEL, "a label is outside [0, C)");
+  if (h & ERR_COMM) return fail(WHALE_ERR_COMM, "a peer flag wait timed out");
+  return WHALE_OK;
+}
+
+// ============================================================================ introspection
+extern "C" int32_t whale_splitfc_launches_per_step(const whale_splitfc_ctx* ctx) {
+  if (!ctx) return 0;
+  const int extra = ctx->p.es == 4 ? 3 : 0;  // fp32 path: operand transposes
+  return (ctx->p.world == 1 ? 7 : 8) + extra;
+}
+
+extern "C" whale_status_t whale_splitfc_profile_enable(whale_splitfc_ctx* ctx, int32_t enable) {
+  if (!ctx) return fail(WHALE_ERR_INVALID_ARG, "NULL ctx");
+  ctx->profile = enable != 0;
+  return WHALE_OK;
+}
+
+extern "C" whale_status_t whale_splitfc_profile_read(whale_splitfc_ctx* ctx, char* names, size_t names_len,
+                                                     double* total_ms, int64_t* launches, int32_t max_kinds,
+                                                     int32_t* n_kinds) {
+  if (!ctx) return fail(WHALE_ERR_INVALID_ARG, "NULL ctx");
+  for (auto& r : ctx->prof) {
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+    ctx->prof_ms[r.kind] += ms;
+    ctx->prof_n[r.kind] += 1;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  ctx->prof.clear();
+  std::string nm;
+  const int n = std::min<int>(K_NUM, max_kinds);
+  for (int k = 0; k < n; ++k) {
+    if (total_ms) total_ms[k] = ctx->prof_ms[k];
+    if (launches) launches[k] = ctx->prof_n[k];
+    nm += kKindNames[k];
+    if (k + 1 < n) nm += ";";
+    ctx->prof_ms[k] = 0;
+    ctx->prof_n[k] = 0;
+  }
+  if (names && names_len) {
+    strncpy(names, nm.c_str(), names_len - 1);
+    names[names_len - 1] = 0;
+  }
+  if (n_kinds) *n_kinds = n;
+  return WHALE_OK;
+}
+
+extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, char* buf, size_t buf_len) {
+  if (!ctx || !buf) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
+  const Plan& p = ctx->p;
+  auto g = [](const GemmCfg& c) {
+    char b[256];
+    snprintf(b, sizeof(b),
+             "{\"BN\":%d,\"m_blocks\":%d,\"n_blocks\":%d,\"splits\":%d,\"num_kb\":%d,\"kb_per_split\":%d,"
+             "\"tiles\":%d,\"stages\":%d,\"smem\":%d,\"grid\":%d}",
+             c.BN, c.m_blocks, c.n_blocks, c.splits, c.num_kb, c.kb_per_split, c.num_tiles, c.stages, c.smem,
+             c.grid);
+    return std::string(b);
+  };
+  char head[256];
+  snprintf(head, sizeof(head),
+           "{\"rank\":%d,\"world\":%d,\"B\":%lld,\"Bt\":%lld,\"D\":%lld,\"C\":%lld,\"C_r\":%lld,\"o_r\":%lld,"
+           "\"ldp\":%lld,\"sms\":%d,",
+           p.rank, p.world, (long long)p.B, (long long)p.Bt, (long long)p.D, (long long)p.C, (long long)p.Cr,
+           (long long)p.o_r, (long long)p.ldp, p.sms);
+  std::string s = std::string(head) + "\"fwd\":" + g(p.fwd) + ",\"dw\":" + g(p.dw) + ",\"dx\":" + g(p.dx) +
+                  ",\"off_P\":" + std::to_string(p.L.P) + ",\"off_m_tile\":" + std::to_string(p.L.m_tile) +
+                  ",\"off_s_tile\":" + std::to_string(p.L.s_tile) + ",\"off_lse\":" + std::to_string(p.L.lse) +
+                  ",\"off_dxpart\":" + std::to_string(p.L.dxpart) +
+                  ",\"local_bytes\":" + std::to_string(p.L.local_total) +
+                  ",\"symm_bytes\":" + std::to_string(p.L.symm_total) + "}";
+  if (s.size() + 1 > buf_len) return fail(WHALE_ERR_INVALID_ARG, "buffer too small (%zu)", s.size() + 1);
+  memcpy(buf, s.c_str(), s.size() + 1);
+  return WHALE_OK;
+}

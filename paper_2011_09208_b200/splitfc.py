@@ -1,0 +1,136 @@
+"""User-facing split-FC softmax cross-entropy (Whale hybrid strategy).
+
+``SplitFCSoftmaxCE`` owns the device workspaces (torch allocations -- plumbing only) and a
+context of libwhale_splitfc.so; ``forward``/``backward`` are the C-ABI calls on the current
+torch stream.  For world > 1 the symmetric (peer-mapped) buffer comes from
+``torch.distributed._symmetric_memory`` and all exchanges run in the library's own NVLink
+kernels; the process group is used only for the rendezvous and a barrier.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+
+class SplitFCSoftmaxCE:
+    """Class-split FC + softmax-CE over ``world`` ranks (shard r <-> rank r).
+
+    Args:
+        num_classes: C.  feature_dim: D.  local_batch: B (per rank, equal on all ranks).
+        capacity: optional integer capacity weights (hardware-aware uneven split).
+        dtype: torch.bfloat16 (tcgen05 kind::f16) or torch.float32 (kind::tf32).
+        group: torch.distributed process group (None -> world 1).
+    """
+
+    def __init__(self, num_classes: int, feature_dim: int, local_batch: int, capacity=None,
+                 dtype=torch.bfloat16, group=None, device=None):
+        self.C, self.D, self.B = int(num_classes), int(feature_dim), int(local_batch)
+        self.dtype = dtype
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if group is not None:
+            import torch.distributed as dist
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+        self.group = group
+        self.counts, self.offsets = _lib.whale_splitfc_plan(self.C, self.world, capacity)
+        self.C_r, self.o_r = self.counts[self.rank], self.offsets[self.rank]
+        xdt = {torch.bfloat16: _lib.WHALE_BF16, torch.float32: _lib.WHALE_F32}[dtype]
+        q, _keep = _lib.make_desc(self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt)
+        symm_bytes, local_bytes = _lib.whale_splitfc_workspace_size(q)
+        self.workspace = torch.empty(local_bytes, dtype=torch.uint8, device=self.device)
+        peer_ptrs = None
+        self._symm = None
+        if self.world > 1:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(symm_bytes, dtype=torch.uint8, device=self.device)
+            hdl = symm_mem.rendezvous(buf, group=group)
+            buf.zero_()
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=group)
+            peer_ptrs = [int(p) for p in hdl.buffer_ptrs]
+            self._symm = (buf, hdl)
+        self._desc, self._keep = _lib.make_desc(
+            self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt, peer_ptrs, symm_bytes,
+            self.workspace.data_ptr(), local_bytes)
+        self.ctx = _lib.whale_splitfc_create(self._desc)
+        self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
+        self.row_loss = torch.zeros(self.B, dtype=torch.float32, device=self.device)
+
+    # ------------------------------------------------------------------ C-ABI calls
+    def forward(self, x_local: torch.Tensor, labels_local: torch.Tensor, w_shard: torch.Tensor,
+                row_loss: bool = False) -> torch.Tensor:
+        """-> device scalar loss (mean over the global batch).  labels: int32 (int64 is cast)."""
+        self._check_inputs(x_local, w_shard)
+        if labels_local.dtype != torch.int32:
+            labels_local = labels_local.to(torch.int32)
+        self._labels = labels_local.contiguous()  # keep alive until the kernels ran
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.whale_splitfc_forward(self.ctx, x_local.data_ptr(), self._labels.data_ptr(), w_shard.data_ptr(),
+                                   self.loss.data_ptr(), self.row_loss.data_ptr() if row_loss else None, stream)
+        return self.loss
+
+    def backward(self, w_shard: torch.Tensor, dx_local: torch.Tensor | None = None,
+                 dw_shard: torch.Tensor | None = None):
+        """-> (dX_r [B x D] in the operand dtype, dW_r [C_r x D] fp32)."""
+        if dx_local is None:
+            dx_local = torch.empty(self.B, self.D, dtype=self.dtype, device=self.device)
+        if dw_shard is None:
+            dw_shard = torch.empty(self.C_r, self.D, dtype=torch.float32, device=self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.whale_splitfc_backward(self.ctx, w_shard.data_ptr(), dx_local.data_ptr(), dw_shard.data_ptr(), stream)
+        return dx_local, dw_shard
+
+    def check(self):
+        _lib.whale_splitfc_check(self.ctx, torch.cuda.current_stream(self.device).cuda_stream)
+
+    def config(self) -> dict:
+        return _lib.whale_splitfc_config(self.ctx)
+
+    def launches_per_step(self) -> int:
+        return _lib.whale_splitfc_launches_per_step(self.ctx)
+
+    def profile(self, enable: bool):
+        _lib.whale_splitfc_profile_enable(self.ctx, enable)
+
+    def profile_read(self) -> dict:
+        return _lib.whale_splitfc_profile_read(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            _lib.whale_splitfc_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check_inputs(self, x, w):
+        if x.shape != (self.B, self.D) or x.dtype != self.dtype or not x.is_contiguous():
+            raise ValueError(f"x_local must be contiguous {self.dtype} [{self.B}, {self.D}]")
+        if w.shape != (self.C_r, self.D) or w.dtype != self.dtype or not w.is_contiguous():
+            raise ValueError(f"w_shard must be contiguous {self.dtype} [{self.C_r}, {self.D}]")
+
+
+class _SplitFCFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x_local, w_shard, labels, op):
+        ctx.op = op
+        ctx.save_for_backward(w_shard)
+        return op.forward(x_local, labels, w_shard).clone()
+
+    @staticmethod
+    def backward(ctx, grad_loss):
+        (w_shard,) = ctx.saved_tensors
+        dx, dw = ctx.op.backward(w_shard)
+        g = grad_loss.to(torch.float32)
+        return (dx * g.to(dx.dtype)), (dw * g).to(w_shard.dtype), None, None
+
+
+def split_fc_softmax_ce(x_local, w_shard, labels, op: SplitFCSoftmaxCE):
+    """Autograd entry: loss = SplitFC-softmax-CE(x_local, w_shard, labels); dW flows to w_shard.grad."""
+    return _SplitFCFunction.apply(x_local, w_shard, labels, op)
