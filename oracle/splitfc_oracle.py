@@ -141,3 +141,52 @@ def sharded_forward_backward(X_list, W, y, counts, offsets) -> dict:
         "dW_shards": dW_parts,
         "dX_ranks": [dX[starts[i]:starts[i + 1]] for i in range(len(Bs))],
     }
+
+
+# ---------------------------------------------------------------------------------
+# Sampled evaluation for full-size configurations (same definitions, class dimension
+# processed in chunks only to bound memory; max first, then the sum with the final max)
+# ---------------------------------------------------------------------------------
+def row_stats_chunked(X, W, rows=None, chunk: int = 65536):
+    """O3 for the given rows (default all): m_i = max_j Z_ij (pass 1), then
+    s_i = sum_j exp(Z_ij - m_i) (pass 2), lse_i = m_i + ln s_i.  Returns (m, s, lse)."""
+    Xd = _f64(X) if rows is None else _f64(X)[np.asarray(rows)]
+    C = W.shape[0]
+    m = np.full(Xd.shape[0], -np.inf)
+    for a in range(0, C, chunk):
+        m = np.maximum(m, (Xd @ _f64(W[a:a + chunk]).T).max(axis=1))
+    s = np.zeros(Xd.shape[0])
+    for a in range(0, C, chunk):
+        s += np.exp(Xd @ _f64(W[a:a + chunk]).T - m[:, None]).sum(axis=1)
+    return m, s, m + np.log(s)
+
+
+def sampled_rows(X, W, y, rows, chunk: int = 65536) -> dict:
+    """Loss terms l_i and dX rows for a subset of rows of a global batch of size
+    B_tot = len(X) (O4, O5, O6 restricted to rows i in `rows`)."""
+    rows = np.asarray(rows)
+    y = np.asarray(y, dtype=np.int64)
+    Bt = len(y)
+    Xr = _f64(X)[rows]
+    _, _, lse = row_stats_chunked(X, W, rows, chunk)
+    C = W.shape[0]
+    zy = np.einsum("ij,ij->i", Xr, _f64(W[y[rows]]))
+    dX = np.zeros_like(Xr)
+    for a in range(0, C, chunk):
+        Wc = _f64(W[a:a + chunk])
+        Gc = np.exp(Xr @ Wc.T - lse[:, None])
+        own = (y[rows] >= a) & (y[rows] < a + Wc.shape[0])
+        Gc[np.nonzero(own)[0], y[rows][own] - a] -= 1.0
+        dX += (Gc / Bt) @ Wc
+    return {"row_loss": lse - zy, "lse": lse, "dX": dX}
+
+
+def sampled_classes(X, W, y, classes, lse) -> np.ndarray:
+    """dW rows for a subset of classes j: dW_j = sum_i (exp(Z_ij - lse_i) - [y_i = j]) X_i / B_tot
+    (O5, O6); `lse` must be the oracle's lse of every row (row_stats_chunked)."""
+    classes = np.asarray(classes)
+    Xd = _f64(X)
+    y = np.asarray(y, dtype=np.int64)
+    G = np.exp(Xd @ _f64(W[classes]).T - np.asarray(lse)[:, None])
+    G -= (y[:, None] == classes[None, :])
+    return (G / len(y)).T @ Xd

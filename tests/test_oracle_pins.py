@@ -16,6 +16,7 @@ import pytest
 import torch
 
 import oracle
+import oracle.splitfc_oracle
 from oracle import PlanError, plan_shards
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
@@ -303,3 +304,19 @@ def test_paper_sizes_pin_workload():
     assert round((D * C + C) * b / 2 ** 20) == g["fc_mb"]
     assert abs(D * C * b / 2 ** 20 - g["fc_mb"]) < 1.0
     assert round(100 * g["fc_mb"] / (g["fc_mb"] + g["resnet50_mb"]), 1) == g["sync_reduction_pct"]
+
+
+def test_sampled_oracle_agrees_with_full():
+    """The chunked / sampled evaluation used for full-size GPU parity reproduces the pinned
+    full oracle (rows, dX rows, dW rows) to ~1e-15 on small inputs with ragged chunks."""
+    X, W, y = _rand(20, 7, 50, 40, scale=8.0)
+    f = oracle.forward_backward(X, W, y)
+    rows = [0, 5, 19]
+    s = oracle.splitfc_oracle.sampled_rows(X, W, y, rows, chunk=16)
+    np.testing.assert_allclose(s["row_loss"], f["row_loss"][rows], rtol=1e-13)
+    np.testing.assert_allclose(s["dX"], f["dX"][rows], rtol=1e-12, atol=1e-16)
+    _, _, lse = oracle.splitfc_oracle.row_stats_chunked(X, W, chunk=13)
+    np.testing.assert_allclose(lse, f["lse"], rtol=1e-14)
+    cls = [0, 3, 49]
+    np.testing.assert_allclose(oracle.splitfc_oracle.sampled_classes(X, W, y, cls, lse), f["dW"][cls],
+                               rtol=1e-12, atol=1e-17)
