@@ -1,6 +1,7 @@
 // Persistent, warp-specialised tcgen05 GEMM for sm_100a with the split-FC epilogues.
 //
-//   D[M x N] = A[M x K] * B[N x K]^T    (bf16 operands, fp32 accumulator in TMEM)
+//   D[M x N] = A[M x K] * B[N x K]^T    (bf16 operands -> kind::f16, or fp32 -> kind::tf32;
+//                                         fp32 accumulator in TMEM)
 //
 // A and B are each either K-major (K contiguous) or MN-major (M/N contiguous); both are
 // fed by TMA into 128B-swizzled shared memory and consumed by tcgen05.mma issued from one
@@ -16,10 +17,18 @@
 //   EPI_FWD_STATS  split-FC forward (north star (b)): the logits tile
 //                  Z = X W_r^T never leaves the SM as fp32.  Per row and class tile the
 //                  epilogue writes m_tile = max_j z, s_tile = sum_j exp(z - m_tile),
-//                  P~ = exp(z - m_tile) (bf16, TMA store) and captures the label logit
-//                  z_y when the label falls in this tile.
-//   EPI_STORE_F32  fp32 tile store through a swizzled smem stage + TMA (3-D map:
+//                  P~ = exp(z - m_tile) (bf16 / fp32, TMA store) and captures the label
+//                  logit z_y when the label falls in this tile.
+//   EPI_STORE_F32  fp32 tile store through swizzled smem stages + TMA (3-D map
 //                  {N, M, split}); used for dW (A7) and the split-K dX partials (A8).
+//                  With fix_mode != 0 (dX) the split-K partials are reduced in a fixed
+//                  split order inside this kernel (all CTAs co-resident -> each reduces
+//                  1/S of its tile after a counter barrier) and the result is either
+//                  written as the final dX (N = 1) or pushed over NVLink into the owner
+//                  rank's receive slab (N > 1, fused GEMM -> reduce-scatter).
+//
+// All kernels use programmatic dependent launch: the prologue (barrier init, TMEM alloc,
+// descriptor prefetch) overlaps the previous kernel's tail.
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -29,6 +38,7 @@
 namespace whale {
 
 enum EpiKind : int { EPI_FWD_STATS = 0, EPI_STORE_F32 = 1 };
+enum FixMode : int { FIX_NONE = 0, FIX_LOCAL = 1, FIX_PUSH = 2 };
 
 constexpr int kBM = 128;               // MMA M (rows of A per tile)
 constexpr int kRowBytes = 128;         // one SWIZZLE_128B row: K elements per stage = 128 / ES
@@ -36,7 +46,6 @@ constexpr int kMaxBN = 256;            // accumulator columns per TMEM buffer
 constexpr int kGemmThreads = 256;      // 8 warps
 constexpr int kStageABytes = kBM * kRowBytes;   // 16 KB
 constexpr int kEpiBufBytes = 4096;     // per epilogue warp per buffer: 32 rows x 128 B
-constexpr int kEpiBytes = 4 * 2 * kEpiBufBytes;
 constexpr int kTmemCols = 512;
 
 struct GemmArgs {
@@ -47,6 +56,9 @@ struct GemmArgs {
   int num_tiles;
   int stages;
   int stage_bytes;
+  int epi_bufs;             // smem store buffers per epilogue warp (2, 4 or 8)
+  int bk;                   // K elements per stage: 128/ES, or 32 (bf16) when both operands are
+                            // MN-major and K is short (dW at small B_tot)
   // EPI_FWD_STATS
   const int32_t* labels;    // [M] global class ids
   long long class_offset;   // first class of this shard
@@ -57,11 +69,25 @@ struct GemmArgs {
   const uint32_t* wait_flags;  // [wait_count] local flag words, NULL = no wait
   int wait_count;
   uint32_t wait_epoch;
+  // split-K fixup (EPI_STORE_F32, dX)
+  int fix_mode;             // FixMode
+  const float* part;        // [splits x M x N] fp32 partials (the tmOut tensor)
+  uint32_t* tile_cnt;       // [m_blocks x n_blocks] monotonic arrival counters
+  uint32_t* done_cnt;       // monotonic count of reduced tile shares
+  uint32_t epoch;           // launch epoch (counters reach epoch * splits)
+  void* out;                // FIX_LOCAL: final dX [M x N] (ES-sized elements)
+  int B, rank, world;       // FIX_PUSH: rows r*B..(r+1)*B belong to rank r
+  PeerPtrs recv;            // FIX_PUSH: owner's fp32 slab [world][B x N] (this parity)
+  PeerFlags rs_flags;       // FIX_PUSH: &flag[RS][rank] on every rank
+  int store_mode;           // EPI_STORE_F32: 0 per-warp TMA box, 1 CTA-wide TMA box, 2 st.global
+  int n_fastest;            // tile order: 0 = M fastest (share B), 1 = N fastest (share A)
+  int debug;                // timing experiments only: bit0 skip stores, bit1 skip TMEM loads
+  float* st_out;            // store_mode 2: output base ([splits x] M x N fp32)
   int* err;
 };
 
-__host__ __device__ inline int gemm_smem_bytes(int stages, int stage_bytes) {
-  return 1024 /*align slack*/ + stages * stage_bytes + kEpiBytes + 256 /*barriers*/;
+__host__ __device__ inline int gemm_smem_bytes(int stages, int stage_bytes, int epi_bufs) {
+  return 1024 /*align slack*/ + stages * stage_bytes + 4 * epi_bufs * kEpiBufBytes + 256 /*barriers*/;
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -77,12 +103,68 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 __device__ __forceinline__ void decode_tile(const GemmArgs& a, int tile, int& mb, int& nb, int& sp, int& kb0,
                                             int& kb1) {
-  mb = tile % a.m_blocks;
-  const int r = tile / a.m_blocks;
-  nb = r % a.n_blocks;
-  sp = r / a.n_blocks;
+  if (a.n_fastest) {
+    nb = tile % a.n_blocks;
+    const int r = tile / a.n_blocks;
+    mb = r % a.m_blocks;
+    sp = r / a.m_blocks;
+  } else {
+    mb = tile % a.m_blocks;
+    const int r = tile / a.m_blocks;
+    nb = r % a.n_blocks;
+    sp = r / a.n_blocks;
+  }
   kb0 = sp * a.kb_per_split;
   kb1 = min(kb0 + a.kb_per_split, a.num_kb);
+}
+
+// Wait until <= n bulk stores of this thread are still reading smem (n = bufs - 1).
+__device__ __forceinline__ void bulk_wait_read_n(int bufs) {
+  if (bufs >= 8) bulk_wait_read<7>();
+  else if (bufs >= 4) bulk_wait_read<3>();
+  else bulk_wait_read<1>();
+}
+
+// Split-K fixup share of one tile (called by the 128 epilogue threads of every CTA that
+// contributed split `sp`, after all splits arrived): reduce partials[0..S) in split order.
+template <int ES>
+__device__ __forceinline__ void fixup_share(const GemmArgs& a, int mb, int nb, int sp, int tid) {
+  const int r0 = mb * kBM;
+  const int nrows = min(kBM, a.M - r0);
+  const int c0 = nb * a.BN;
+  const int nc4 = min(a.BN, a.N - c0) / 4;
+  const int total = nrows * nc4;
+  const int per = (total + a.splits - 1) / a.splits;
+  const int e0 = sp * per, e1 = min(total, e0 + per);
+  const size_t split_stride = static_cast<size_t>(a.M) * a.N;
+  for (int e = e0 + tid; e < e1; e += 128) {
+    const int r = r0 + e / nc4;
+    const int c = c0 + (e % nc4) * 4;
+    const float* src = a.part + static_cast<size_t>(r) * a.N + c;
+    float4 acc = __ldcg(reinterpret_cast<const float4*>(src));
+    for (int s = 1; s < a.splits; ++s) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(src + s * split_stride));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    if (a.fix_mode == FIX_LOCAL) {
+      if constexpr (ES == 2) {
+        uint2 o;
+        o.x = pack_bf16x2(acc.x, acc.y);
+        o.y = pack_bf16x2(acc.z, acc.w);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + static_cast<size_t>(r) * a.N + c) = o;
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + static_cast<size_t>(r) * a.N + c) = acc;
+      }
+    } else {
+      const int owner = r / a.B;
+      float* dst = reinterpret_cast<float*>(a.recv.p[owner]) +
+                   (static_cast<size_t>(a.rank) * a.B + (r - owner * a.B)) * a.N + c;
+      *reinterpret_cast<float4*>(dst) = acc;  // NVLink store into the owner's slab
+    }
+  }
 }
 
 // ES = operand element size: 2 -> bf16 (kind::f16), 4 -> fp32 storage run as kind::tf32.
@@ -91,9 +173,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     splitfc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmOut, const GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_fix_go;
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* epi_smem = smem + a.stages * a.stage_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + 4 * a.epi_bufs * kEpiBufBytes);
   uint64_t* empty = full + a.stages;
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 2;
@@ -101,7 +184,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   constexpr int kBK = kRowBytes / ES;        // K elements per stage
   constexpr int kAtom = kRowBytes / ES;      // MN elements per swizzle atom (MN-major)
-  constexpr int kBoxBytes = kBK * kRowBytes; // one MN-major box {kAtom, kBK}
   constexpr int kKStepMN = (32 / ES) * kRowBytes;  // MN-major: UMMA_K rows per MMA
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -127,6 +209,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_wait();      // everything below reads/writes memory the previous kernel may touch
+  pdl_trigger();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -139,27 +223,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       int stage = 0;
       uint32_t phase = 0;
-      const uint32_t tx = static_cast<uint32_t>(kStageABytes + a.BN * kRowBytes);
+      const int bk = (A_MN && B_MN) ? a.bk : kBK;
+      const int box_bytes = bk * kRowBytes;
+      const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
+      const uint32_t tx = static_cast<uint32_t>(a_bytes + (B_MN ? (a.BN / kAtom) * box_bytes : a.BN * kRowBytes));
       for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
         int mb, nb, sp, kb0, kb1;
         decode_tile(a, tile, mb, nb, sp, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* sA = smem + stage * a.stage_bytes;
-          uint8_t* sB = sA + kStageABytes;
+          uint8_t* sB = sA + a_bytes;
           mbar_arrive_expect_tx(&full[stage], tx);
           if (!A_MN) {
             tma_load_2d(sA, &tmA, &full[stage], kb * kBK, mb * kBM);
           } else {
 #pragma unroll
             for (int j = 0; j < kBM / kAtom; ++j)
-              tma_load_2d(sA + j * kBoxBytes, &tmA, &full[stage], mb * kBM + j * kAtom, kb * kBK);
+              tma_load_2d(sA + j * box_bytes, &tmA, &full[stage], mb * kBM + j * kAtom, kb * bk);
           }
           if (!B_MN) {
             tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
           } else {
             for (int j = 0; j < a.BN / kAtom; ++j)
-              tma_load_2d(sB + j * kBoxBytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * kBK);
+              tma_load_2d(sB + j * box_bytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * bk);
           }
           if (++stage == a.stages) {
             stage = 0;
@@ -172,6 +259,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // ===================== MMA issuer =====================
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(kBM, a.BN, A_MN, B_MN, ES == 2 ? 1u : 2u);
+      const int bk = (A_MN && B_MN) ? a.bk : kBK;
+      const uint32_t box_bytes = bk * kRowBytes;
+      const uint32_t a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
+      const int kmma = bk / (32 / ES);  // MMAs (32 bytes of K each) per stage
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -187,12 +278,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t aS = smem_u32(smem + stage * a.stage_bytes);
-          const uint32_t bS = aS + kStageABytes;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 4 MMAs x 32 bytes of K per 128-byte row
-            const uint64_t ad = A_MN ? umma_sdesc(aS + k * kKStepMN, kBoxBytes, 1024)
+          const uint32_t bS = aS + a_bytes;
+#pragma unroll 4
+          for (int k = 0; k < kmma; ++k) {  // MMAs of 32 bytes of K
+            const uint64_t ad = A_MN ? umma_sdesc(aS + k * kKStepMN, box_bytes, 1024)
                                      : umma_sdesc(aS + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? umma_sdesc(bS + k * kKStepMN, kBoxBytes, 1024)
+            const uint64_t bd = B_MN ? umma_sdesc(bS + k * kKStepMN, box_bytes, 1024)
                                      : umma_sdesc(bS + k * 32, 16, 1024);
             if constexpr (ES == 2)
               umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
@@ -211,7 +302,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    uint8_t* ebuf = epi_smem + q * 2 * kEpiBufBytes;
+    const int nbuf = a.epi_bufs;
+    uint8_t* ebuf = epi_smem + q * nbuf * kEpiBufBytes;
     int buf = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
@@ -224,13 +316,70 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t tbase = tmem_base + acc * kMaxBN + (static_cast<uint32_t>(q * 32) << 16);
       const int row0 = mb * kBM + q * 32;  // first output row of this warp
       const int row = row0 + lane;
-      if (row0 < a.M) {  // warp-uniform: skip warps whose rows are all padding
-        if constexpr (EPI == EPI_STORE_F32) {
+      if constexpr (EPI == EPI_STORE_F32) {
+        if (a.store_mode == 1) {
+          // CTA-wide 128-row box: all 4 warps fill one 16 KB stage, one thread stores it
+          for (int c0 = 0; c0 < a.BN; c0 += 32) {
+            uint32_t v[32];
+            if (!(a.debug & 2)) {
+              tmem_ld32(tbase + c0, v);
+              tmem_ld_wait();
+            } else {
+#pragma unroll
+              for (int k = 0; k < 32; ++k) v[k] = k;
+            }
+            if (c0 + 32 >= a.BN) {
+              tc_fence_before();
+              mbar_arrive(&tempty[acc]);
+            }
+            if (a.debug & 1) continue;
+            if (threadIdx.x == 128) bulk_wait_read_n(nbuf);
+            named_bar_sync(1, 128);
+            uint8_t* b = epi_smem + buf * 4 * kEpiBufBytes + (q * 32 + lane) * 128;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch)
+              *reinterpret_cast<uint4*>(b + ((ch ^ (lane & 7)) << 4)) =
+                  make_uint4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+            fence_proxy_async_smem();
+            named_bar_sync(1, 128);
+            if (threadIdx.x == 128) {
+              tma_store_3d(&tmOut, epi_smem + buf * 4 * kEpiBufBytes, nb * a.BN + c0, mb * kBM, sp);
+              bulk_commit();
+            }
+            if (++buf == nbuf) buf = 0;
+          }
+        } else if (a.store_mode == 2) {
+          // direct 16-byte global stores from registers (each thread: its row, 128 B per chunk)
+          const bool rv = row < a.M;
+          float* orow = a.st_out + (static_cast<size_t>(sp) * a.M + (rv ? row : 0)) * a.N;
           for (int c0 = 0; c0 < a.BN; c0 += 32) {
             uint32_t v[32];
             tmem_ld32(tbase + c0, v);
             tmem_ld_wait();
-            if (lane == 0) bulk_wait_read<1>();  // the store that last used this buffer has read it
+            if (c0 + 32 >= a.BN) {
+              tc_fence_before();
+              mbar_arrive(&tempty[acc]);
+            }
+            const int col = nb * a.BN + c0;
+            if (rv) {
+#pragma unroll
+              for (int ch = 0; ch < 8; ++ch)
+                if (col + 4 * ch < a.N)
+                  __stcs(reinterpret_cast<float4*>(orow + col + 4 * ch),
+                         make_float4(__uint_as_float(v[4 * ch]), __uint_as_float(v[4 * ch + 1]),
+                                     __uint_as_float(v[4 * ch + 2]), __uint_as_float(v[4 * ch + 3])));
+            }
+          }
+        } else if (row0 < a.M) {
+          for (int c0 = 0; c0 < a.BN; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tbase + c0, v);
+            tmem_ld_wait();
+            if (c0 + 32 >= a.BN) {  // accumulator fully read: hand TMEM back to the MMA warp
+              tc_fence_before();
+              mbar_arrive(&tempty[acc]);
+            }
+            if (lane == 0) bulk_wait_read_n(nbuf);  // the store that last used this buffer has read it
             __syncwarp();
             uint8_t* b = ebuf + buf * kEpiBufBytes + lane * 128;
 #pragma unroll
@@ -243,9 +392,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               tma_store_3d(&tmOut, ebuf + buf * kEpiBufBytes, nb * a.BN + c0, row0, sp);
               bulk_commit();
             }
-            buf ^= 1;
+            if (++buf == nbuf) buf = 0;
           }
         } else {
+          tc_fence_before();
+          mbar_arrive(&tempty[acc]);
+        }
+      } else if (row0 < a.M) {  // warp-uniform: skip warps whose rows are all padding
+        {
           const bool rv = row < a.M;
           const int ncol = min(a.BN, a.N - nb * a.BN);  // valid classes in this tile
           constexpr float kLog2e = 1.4426950408889634f;
@@ -270,6 +424,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tmem_ld32(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
             if constexpr (kChunk == 64) tmem_ld32(tbase + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
             tmem_ld_wait();
+            if (c0 + kChunk >= a.BN) {
+              tc_fence_before();
+              mbar_arrive(&tempty[acc]);
+            }
             uint32_t pk[32];
 #pragma unroll
             for (int c = 0; c < kChunk; c += 2) {
@@ -287,7 +445,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 pk[c + 1] = __float_as_uint(p1);
               }
             }
-            if (lane == 0) bulk_wait_read<1>();
+            if (lane == 0) bulk_wait_read_n(nbuf);
             __syncwarp();
             uint8_t* b = ebuf + buf * kEpiBufBytes + lane * 128;
 #pragma unroll
@@ -300,7 +458,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               tma_store_2d(&tmOut, ebuf + buf * kEpiBufBytes, nb * a.BN + c0, row0);
               bulk_commit();
             }
-            buf ^= 1;
+            if (++buf == nbuf) buf = 0;
           }
           if (rv) {
             a.m_tile[static_cast<size_t>(row) * a.n_blocks + nb] = mx;
@@ -308,9 +466,45 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (yl >= 0 && yl < ncol) a.zy[row] = zy;
           }
         }
+      } else {
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (EPI == EPI_STORE_F32) {
+        if (a.fix_mode != FIX_NONE) {
+          // ---- split-K fixup: publish this split, wait for all, reduce my 1/S share ----
+          if (lane == 0 || threadIdx.x == 128) bulk_wait<0>();  // this CTA's partial stores are complete
+          __syncwarp();
+          fence_proxy_async_global();
+          __threadfence();
+          named_bar_sync(1, 128);
+          uint32_t* cnt = a.tile_cnt + mb * a.n_blocks + nb;
+          if (threadIdx.x == 128) {
+            atomicAdd(cnt, 1u);
+            const uint32_t target = a.epoch * static_cast<uint32_t>(a.splits);
+            if (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0) {
+              SpinGuard g;
+              while (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0) g.check(a.err, 16);
+            }
+          }
+          named_bar_sync(1, 128);
+          __threadfence();
+          fixup_share<ES>(a, mb, nb, sp, threadIdx.x - 128);
+          if (a.fix_mode == FIX_PUSH) {
+            __threadfence_system();
+            named_bar_sync(1, 128);
+            if (threadIdx.x == 128) {
+              const uint32_t done = atomicAdd(a.done_cnt, 1u) + 1u;
+              s_fix_go = (done == a.epoch * static_cast<uint32_t>(a.num_tiles));
+            }
+            named_bar_sync(1, 128);
+            if (s_fix_go) {  // every share of every tile is in its owner's slab: signal
+              __threadfence_system();
+              if (threadIdx.x - 128 < a.world) st_release_sys(a.rs_flags.p[threadIdx.x - 128], a.epoch);
+            }
+          }
+        }
+      }
     }
     if (lane == 0) bulk_wait<0>();
   }

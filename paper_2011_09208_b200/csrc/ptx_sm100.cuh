@@ -214,6 +214,30 @@ __device__ __forceinline__ void wait_flag_geq(const uint32_t* p, uint32_t epoch,
   while (static_cast<int32_t>(ld_acquire_sys(p) - epoch) < 0) g.check(err_word, code);
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Programmatic dependent launch: wait for the preceding grid's memory, and let the next
+// grid be scheduled early (its own griddepcontrol.wait keeps it correct).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Named barrier over a subset of warps (id > 0; id 0 is __syncthreads).
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+constexpr int kMaxRanks = 8;
+struct PeerPtrs {
+  void* p[kMaxRanks];
+};
+struct PeerFlags {
+  uint32_t* p[kMaxRanks];
+};
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

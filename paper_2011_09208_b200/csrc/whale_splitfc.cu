@@ -83,22 +83,23 @@ extern "C" whale_status_t whale_splitfc_plan(int64_t num_classes, int32_t world_
 
 // ============================================================================ configuration
 struct GemmCfg {
-  int BN = 0, m_blocks = 0, n_blocks = 0, splits = 1, num_kb = 0, kb_per_split = 0, num_tiles = 0;
-  int stages = 0, stage_bytes = 0, smem = 0, grid = 0;
+  int BN = 0, bk = 64, m_blocks = 0, n_blocks = 0, splits = 1, num_kb = 0, kb_per_split = 0, num_tiles = 0;
+  int stages = 0, stage_bytes = 0, epi_bufs = 2, smem = 0, grid = 0;
 };
 
 struct Layout {
   // local workspace offsets
-  size_t P, m_tile, s_tile, zy, lse, row_loss, stats_local, dxpart, xg_local, yg_local, counters, local_total;
+  size_t P = 0, m_tile = 0, s_tile = 0, zy = 0, lse = 0, row_loss = 0, dxpart = 0, counters = 0, tile_cnt = 0;
+  size_t local_total = 0;
   // fp32 (kind::tf32) backward only: K-major transposed operands
   size_t XT = 0, GT = 0, WT = 0;
   int64_t ld_bt = 0;
-  // symmetric buffer offsets (per parity for the slabs)
-  size_t flags, xg[2], yg[2], stats[2], dxrecv[2], symm_total;
+  // symmetric buffer offsets (per parity for the slabs); world > 1 only
+  size_t flags = 0, xg[2] = {0, 0}, yg[2] = {0, 0}, stats[2] = {0, 0}, dxrecv[2] = {0, 0}, symm_total = 0;
 };
 
 enum FlagKind { FLAG_GATHER = 0, FLAG_STATS = 1, FLAG_RS = 2 };
-enum CounterIdx { CNT_GATHER = 0, CNT_STATS = 1, CNT_RS = 2, CNT_ERR = 16 };
+enum CounterIdx { CNT_GATHER = 0, CNT_STATS = 1, CNT_DONE = 2, CNT_ERR = 16 };
 
 struct Plan {
   int rank = 0, world = 1, es = 2;
@@ -108,15 +109,29 @@ struct Plan {
   Layout L;
 };
 
-static constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100
+static constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100 (static + dynamic)
+static constexpr int kStaticSmemSlack = 128;  // the GEMM's own __shared__ words
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 static int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
 
-static void finish_cfg(GemmCfg& g, int sms) {
-  g.stage_bytes = kStageABytes + g.BN * kRowBytes;
-  g.stages = std::min(8, (kSmemLimit - 1024 - kEpiBytes - 256) / g.stage_bytes);
-  g.smem = gemm_smem_bytes(g.stages, g.stage_bytes);
+// Stages / store buffers: short K loops (dW: K = B_tot) are store-bound -> deep store
+// pipelining (8 x 4 KB in flight per epilogue warp); long K loops keep 4+ load stages.
+static void finish_cfg(GemmCfg& g, int sms, bool store_heavy, int es = 2, bool both_mn = false) {
+  if (both_mn) {  // MN-major boxes {atom, bk}: A = 128/atom boxes, B = BN/atom boxes
+    const int atom = kRowBytes / es;
+    g.stage_bytes = (kBM / atom + g.BN / atom) * g.bk * kRowBytes;
+  } else {
+    g.stage_bytes = kStageABytes + g.BN * kRowBytes;
+  }
+  g.epi_bufs = store_heavy ? 8 : 2;
+  const int avail = kSmemLimit - kStaticSmemSlack - 1024 - 256 - 4 * g.epi_bufs * kEpiBufBytes;
+  g.stages = std::min(8, avail / g.stage_bytes);
+  if (g.stages < 2) {
+    g.epi_bufs = 2;
+    g.stages = std::min(8, (kSmemLimit - kStaticSmemSlack - 1024 - 256 - 4 * 2 * kEpiBufBytes) / g.stage_bytes);
+  }
+  g.smem = gemm_smem_bytes(g.stages, g.stage_bytes, g.epi_bufs);
   g.num_tiles = g.m_blocks * g.n_blocks * g.splits;
   g.grid = std::min(g.num_tiles, sms);
 }
@@ -141,12 +156,13 @@ static GemmCfg choose_plain(int64_t M, int64_t N, int64_t K, int gran, int kbk, 
       best = g;
     }
   }
-  finish_cfg(best, sms);
+  finish_cfg(best, sms, best.num_kb <= 4);
   return best;
 }
 
-// dX: M = B_tot, N = D, K = C_r.  Split K so that tiles fill the SMs; partial sums go to
-// an fp32 [S x B_tot x D] buffer that the reduce-scatter sums in a fixed order.
+// dX: M = B_tot, N = D, K = C_r.  Split K so that tiles fill the SMs; the partial sums
+// ([S x B_tot x D] fp32) are reduced inside the kernel (fixup), which needs every CTA of a
+// tile co-resident: S > 1 only when all tiles fit in one wave.
 static GemmCfg choose_splitk(int64_t M, int64_t N, int64_t K, int gran, int kbk, int sms) {
   GemmCfg best;
   double best_cost = 1e300;
@@ -157,9 +173,9 @@ static GemmCfg choose_splitk(int64_t M, int64_t N, int64_t K, int gran, int kbk,
     const int64_t mn = static_cast<int64_t>(mb) * nb;
     for (int S = 1; S <= std::min(num_kb, 64); ++S) {
       const int kbps = cdiv(num_kb, S);
-      const int Sr = cdiv(num_kb, kbps);
-      if (Sr != S) continue;
+      if (cdiv(num_kb, kbps) != S) continue;
       const int64_t tiles = mn * S;
+      if (S > 1 && tiles > sms) break;
       const double kblock_bytes = (128.0 + BN) * kRowBytes;
       const double cost = static_cast<double>(cdiv(tiles, sms)) * kbps * kblock_bytes +
                           static_cast<double>(S) * M * N * 8.0 / sms;
@@ -176,7 +192,7 @@ static GemmCfg choose_splitk(int64_t M, int64_t N, int64_t K, int gran, int kbk,
       }
     }
   }
-  finish_cfg(best, sms);
+  finish_cfg(best, sms, false);
   return best;
 }
 
@@ -215,7 +231,14 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   const int kbk = kRowBytes / p.es;   // K elements per stage
   const int atom = kRowBytes / p.es;  // MN-major atom / fwd P~ chunk
   p.fwd = choose_plain(p.Bt, p.Cr, p.D, atom, kbk, sms);
-  p.dw = choose_plain(p.Cr, p.D, p.Bt, atom, kbk, sms);
+  {
+    // dW: both operands MN-major; a short K (= B_tot <= 32) uses 32-row K stages (no
+    // zero-padded half stage), which doubles the pipeline depth for the same smem.
+    const int bk = (p.es == 2 && p.Bt <= 32) ? 32 : kbk;
+    p.dw = choose_plain(p.Cr, p.D, p.Bt, atom, bk, sms);
+    p.dw.bk = bk;
+    finish_cfg(p.dw, sms, p.dw.num_kb <= 4, p.es, p.es == 2);
+  }
   p.dx = choose_splitk(p.Bt, p.D, p.Cr, atom, kbk, sms);
 
   Layout& L = p.L;
@@ -232,11 +255,9 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   L.zy = take(p.Bt * 4);
   L.lse = take(p.Bt * 4);
   L.row_loss = take(p.Bt * 4);
-  L.stats_local = take(p.Bt * 16);
   L.dxpart = take(static_cast<size_t>(p.dx.splits) * p.Bt * p.D * 4);
-  L.xg_local = take(p.world == 1 ? static_cast<size_t>(p.Bt) * p.D * p.es : 0);
-  L.yg_local = take(p.world == 1 ? p.Bt * 4 : 0);
   L.counters = take(64 * 4);
+  L.tile_cnt = take(static_cast<size_t>(p.dx.m_blocks) * p.dx.n_blocks * 4);
   if (p.es == 4) {
     L.ld_bt = static_cast<int64_t>(align_up(p.Bt, 4));
     L.XT = take(static_cast<size_t>(p.D) * L.ld_bt * 4);
@@ -318,10 +339,16 @@ static whale_status_t map2d(CUtensorMap* m, const void* base, int es, uint64_t i
   return make_map(m, base, es, 2, dims, strides, box);
 }
 
+static int g_store_mode = [] {
+  const char* e = getenv("WHALE_STORE_MODE");
+  return e ? atoi(e) : 1;
+}();
+
+// fp32 output map {N, rows, splits}; box rows = 128 for the CTA-wide store (mode 1), else 32.
 static whale_status_t map3d_f32(CUtensorMap* m, const void* base, uint64_t n, uint64_t rows, uint64_t splits) {
   const uint64_t dims[3] = {n, rows, splits};
   const uint64_t strides[2] = {n * 4, n * rows * 4};
-  const uint32_t box[3] = {32, 32, 1};
+  const uint32_t box[3] = {32, g_store_mode == 1 ? 128u : 32u, 1};
   return make_map(m, base, 4, 3, dims, strides, box);
 }
 
@@ -331,23 +358,28 @@ struct ProfRec {
   cudaEvent_t a, b;
 };
 static const char* kKindNames[] = {"bridge_gather", "logits_gemm", "stats_combine", "softmax_grad",
-                                   "dw_gemm",       "dx_gemm",     "dx_rs_push",    "dx_rs_reduce"};
-enum KernelKind { K_GATHER, K_LOGITS, K_STATS, K_GRAD, K_DW, K_DX, K_RS_PUSH, K_RS_REDUCE, K_NUM };
+                                   "dw_gemm",       "dx_gemm",     "dx_rs_reduce",  "transpose_f32"};
+enum KernelKind { K_GATHER, K_LOGITS, K_STATS, K_GRAD, K_DW, K_DX, K_RS_REDUCE, K_TRANSPOSE, K_NUM };
 
 struct whale_splitfc_ctx {
   Plan p;
   uint8_t* ws = nullptr;
   uint8_t* symm[kMaxRanks] = {};
-  // static maps
+  // static maps (X maps: per parity at N > 1; cached on the caller's X at N = 1)
   CUtensorMap tmX_fwd[2], tmX_dw[2], tmP_store, tmG_dx, tmG_dw, tmDxPart;
   CUtensorMap tmGT, tmXT, tmWT;  // fp32 path: K-major transposed operands
   // pointer-cached maps
+  const void* x_cached = nullptr;
   const void* w_cached = nullptr;
   CUtensorMap tmW_fwd, tmW_dx;
   const void* dw_cached = nullptr;
   CUtensorMap tmDW;
-  uint32_t epoch = 0;
+  const void* x_fwd = nullptr;       // N = 1: the forward's X (read again by dW)
+  const int32_t* y_fwd = nullptr;    // N = 1: the forward's labels
+  uint32_t epoch = 0;                // forward count (flag epochs, parity)
+  uint32_t bwd_epoch = 0;            // backward count (fixup counters)
   bool have_fwd = false;
+  bool pdl = true;
   bool profile = false;
   std::vector<ProfRec> prof;
   double prof_ms[K_NUM] = {};
@@ -359,6 +391,24 @@ static T* wsp(whale_splitfc_ctx* c, size_t off) {
   return reinterpret_cast<T*>(c->ws + off);
 }
 
+// Launch with programmatic dependent launch (PDL): kernels call griddepcontrol.wait.
+template <typename... KArgs, typename... Args>
+static whale_status_t launch(whale_splitfc_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->pdl ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+  return WHALE_OK;
+}
+
 static bool g_attr_done[8] = {};
 
 template <int EPI, bool AMN, bool BMN, int ES>
@@ -367,12 +417,13 @@ static whale_status_t launch_gemm(whale_splitfc_ctx* c, int slot, const GemmCfg&
                                   cudaStream_t s) {
   auto kern = splitfc_gemm_kernel<EPI, AMN, BMN, ES>;
   if (!g_attr_done[slot]) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit));
+    cudaFuncAttributes fa{};
+    CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
     g_attr_done[slot] = true;
   }
-  kern<<<g.grid, kGemmThreads, g.smem, s>>>(A, B, O, args);
-  CUDA_TRY(cudaGetLastError());
-  return WHALE_OK;
+  return launch(c, kern, dim3(g.grid), dim3(kGemmThreads), g.smem, s, A, B, O, args);
 }
 
 static void prof_begin(whale_splitfc_ctx* c, int kind, cudaStream_t s, ProfRec& r) {
@@ -397,6 +448,13 @@ static void prof_end(whale_splitfc_ctx* c, cudaStream_t s, ProfRec& r) {
     prof_end(c, stream, _r);                    \
   } while (0)
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+static int g_n_fastest = env_int("WHALE_N_FASTEST", 0);
+static int g_epi_debug = env_int("WHALE_EPI_DEBUG", 0);
+
 static GemmArgs base_args(const GemmCfg& g, int M, int N) {
   GemmArgs a{};
   a.M = M;
@@ -410,8 +468,22 @@ static GemmArgs base_args(const GemmCfg& g, int M, int N) {
   a.num_tiles = g.num_tiles;
   a.stages = g.stages;
   a.stage_bytes = g.stage_bytes;
+  a.epi_bufs = g.epi_bufs;
+  a.bk = g.bk;
+  a.store_mode = g_store_mode;
+  a.n_fastest = g_n_fastest;
+  a.debug = g_epi_debug;
   return a;
 }
+
+#define MAP_TRY(x)                 \
+  do {                             \
+    whale_status_t _s = (x);       \
+    if (_s != WHALE_OK) {          \
+      delete c;                    \
+      return _s;                   \
+    }                              \
+  } while (0)
 
 extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, whale_splitfc_ctx** out) {
   if (!out) return fail(WHALE_ERR_INVALID_ARG, "NULL out");
@@ -441,26 +513,21 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     }
     for (int r = 0; r < p.world; ++r) c->symm[r] = static_cast<uint8_t*>(desc->peer_symm_ptrs[r]);
   }
+  const char* pdl_env = getenv("WHALE_PDL");
+  c->pdl = !(pdl_env && pdl_env[0] == '0');
   // static TMA maps
   const int es = p.es, kbk = kRowBytes / es, atom = kRowBytes / es;
-  for (int par = 0; par < 2; ++par) {
-    const void* xg = p.world == 1 ? static_cast<const void*>(c->ws + p.L.xg_local)
-                                  : static_cast<const void*>(c->symm[p.rank] + p.L.xg[par]);
-#define MAP_TRY(x)                 \
-  do {                             \
-    whale_status_t _s = (x);       \
-    if (_s != WHALE_OK) {          \
-      delete c;                    \
-      return _s;                   \
-    }                              \
-  } while (0)
-    MAP_TRY(map2d(&c->tmX_fwd[par], xg, es, p.D, p.Bt, p.D * es, kbk, kBM));
-    MAP_TRY(map2d(&c->tmX_dw[par], xg, es, p.D, p.Bt, p.D * es, atom, kbk));
+  if (p.world > 1) {
+    for (int par = 0; par < 2; ++par) {
+      const void* xg = c->symm[p.rank] + p.L.xg[par];
+      MAP_TRY(map2d(&c->tmX_fwd[par], xg, es, p.D, p.Bt, p.D * es, kbk, kBM));
+      MAP_TRY(map2d(&c->tmX_dw[par], xg, es, p.D, p.Bt, p.D * es, atom, p.dw.bk));
+    }
   }
   void* P = c->ws + p.L.P;
   MAP_TRY(map2d(&c->tmP_store, P, es, p.Cr, p.Bt, p.ldp * es, kRowBytes / es, 32));
   MAP_TRY(map2d(&c->tmG_dx, P, es, p.Cr, p.Bt, p.ldp * es, kbk, kBM));
-  MAP_TRY(map2d(&c->tmG_dw, P, es, p.Cr, p.Bt, p.ldp * es, atom, kbk));
+  MAP_TRY(map2d(&c->tmG_dw, P, es, p.Cr, p.Bt, p.ldp * es, atom, p.dw.bk));
   MAP_TRY(map3d_f32(&c->tmDxPart, c->ws + p.L.dxpart, p.D, p.Bt, p.dx.splits));
   if (es == 4) {
     const int64_t ldb = p.L.ld_bt;
@@ -468,11 +535,12 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     MAP_TRY(map2d(&c->tmXT, c->ws + p.L.XT, 4, p.Bt, p.D, ldb * 4, kbk, p.dw.BN));
     MAP_TRY(map2d(&c->tmWT, c->ws + p.L.WT, 4, p.Cr, p.D, p.ldp * 4, kbk, p.dx.BN));
   }
-#undef MAP_TRY
   CUDA_TRY(cudaMemset(c->ws + p.L.counters, 0, 64 * 4));
+  CUDA_TRY(cudaMemset(c->ws + p.L.tile_cnt, 0, static_cast<size_t>(p.dx.m_blocks) * p.dx.n_blocks * 4));
   *out = c;
   return WHALE_OK;
 }
+#undef MAP_TRY
 
 extern "C" whale_status_t whale_splitfc_destroy(whale_splitfc_ctx* ctx) {
   if (!ctx) return WHALE_OK;
@@ -484,7 +552,6 @@ extern "C" whale_status_t whale_splitfc_destroy(whale_splitfc_ctx* ctx) {
   return WHALE_OK;
 }
 
-// ============================================================================ forward
 // (re)encode the weight maps when the shard pointer changes (host-only, ~us)
 static whale_status_t ensure_w_maps(whale_splitfc_ctx* c, const void* w) {
   if (w == c->w_cached) return WHALE_OK;
@@ -498,54 +565,61 @@ static whale_status_t ensure_w_maps(whale_splitfc_ctx* c, const void* w) {
   return WHALE_OK;
 }
 
+// N = 1: the bridge is the identity -- the GEMMs read the caller's X through maps cached
+// on its pointer (slot 0).
+static whale_status_t ensure_x_maps(whale_splitfc_ctx* c, const void* x) {
+  if (x == c->x_cached) return WHALE_OK;
+  const Plan& p = c->p;
+  const int kbk = kRowBytes / p.es, atom = kRowBytes / p.es;
+  whale_status_t st = map2d(&c->tmX_fwd[0], x, p.es, p.D, p.Bt, p.D * p.es, kbk, kBM);
+  if (st != WHALE_OK) return st;
+  st = map2d(&c->tmX_dw[0], x, p.es, p.D, p.Bt, p.D * p.es, atom, p.dw.bk);
+  if (st != WHALE_OK) return st;
+  c->x_cached = x;
+  return WHALE_OK;
+}
+
+// ============================================================================ forward
 template <int ES>
 static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, const int32_t* y_local,
                                    const void* w, float* loss, float* row_loss, cudaStream_t s) {
   const Plan& p = c->p;
   const Layout& L = p.L;
-  const int par = c->epoch & 1;
+  const int par = p.world == 1 ? 0 : (c->epoch & 1);
   unsigned* counters = wsp<unsigned>(c, L.counters);
   int* err = reinterpret_cast<int*>(counters + CNT_ERR);
-
   {
     whale_status_t st = ensure_w_maps(c, w);
     if (st != WHALE_OK) return st;
   }
-  // ---- A2 bridge all-gather
-  PeerPtrs dx{}, dy{};
-  PeerFlags fl{};
-  void* xg_local_ptr;
-  int32_t* yg_local_ptr;
+  const int32_t* yg;
   if (p.world == 1) {
-    dx.p[0] = c->ws + L.xg_local;
-    dy.p[0] = c->ws + L.yg_local;
-    xg_local_ptr = dx.p[0];
-    yg_local_ptr = static_cast<int32_t*>(dy.p[0]);
+    whale_status_t st = ensure_x_maps(c, x_local);
+    if (st != WHALE_OK) return st;
+    yg = y_local;
+    c->x_fwd = x_local;
+    c->y_fwd = y_local;
   } else {
+    // ---- A2 bridge all-gather over NVLink
+    PeerPtrs dx{}, dy{};
+    PeerFlags fl{};
     for (int r = 0; r < p.world; ++r) {
       dx.p[r] = c->symm[r] + L.xg[par];
       dy.p[r] = c->symm[r] + L.yg[par];
       fl.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_GATHER * kMaxRanks + p.rank;
     }
-    xg_local_ptr = c->symm[p.rank] + L.xg[par];
-    yg_local_ptr = reinterpret_cast<int32_t*>(c->symm[p.rank] + L.yg[par]);
-  }
-  (void)xg_local_ptr;
-  {
+    yg = reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg[par]);
     const int64_t x_vecs = p.B * p.D * ES / 16;
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(x_vecs, 256), 2 * p.sms)));
-    PROFILED(K_GATHER, s, ([&]() -> whale_status_t {
-               bridge_gather_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(x_local), y_local, x_vecs,
-                                                         static_cast<int>(p.B), p.rank, p.world, dx, dy, fl,
-                                                         c->epoch, counters + CNT_GATHER);
-               CUDA_TRY(cudaGetLastError());
-               return WHALE_OK;
-             }()));
+    PROFILED(K_GATHER, s,
+             (launch(c, bridge_gather_kernel, dim3(grid), dim3(256), 0, s, static_cast<const uint4*>(x_local),
+                     y_local, x_vecs, static_cast<int>(p.B), p.rank, p.world, dx, dy, fl, c->epoch,
+                     counters + CNT_GATHER)));
   }
   // ---- A3 logits GEMM with fused row statistics
   {
     GemmArgs a = base_args(p.fwd, static_cast<int>(p.Bt), static_cast<int>(p.Cr));
-    a.labels = yg_local_ptr;
+    a.labels = yg;
     a.class_offset = p.o_r;
     a.m_tile = wsp<float>(c, L.m_tile);
     a.s_tile = wsp<float>(c, L.s_tile);
@@ -560,13 +634,13 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
              (launch_gemm<EPI_FWD_STATS, false, false, ES>(c, ES == 2 ? 0 : 3, p.fwd, c->tmX_fwd[par],
                                                            c->tmW_fwd, c->tmP_store, a, s)));
   }
-  // ---- A4 + A5 statistics exchange, combine, loss
+  // ---- A4 + A5 statistics (exchange), combine, loss
   {
     StatsArgs a{};
     a.m_tile = wsp<float>(c, L.m_tile);
     a.s_tile = wsp<float>(c, L.s_tile);
     a.zy_r = wsp<float>(c, L.zy);
-    a.y = yg_local_ptr;
+    a.y = yg;
     a.T = p.fwd.n_blocks;
     a.Bt = static_cast<int>(p.Bt);
     a.B = static_cast<int>(p.B);
@@ -575,9 +649,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.o_r = p.o_r;
     a.C_r = p.Cr;
     a.C = p.C;
-    if (p.world == 1) {
-      a.my_stats = wsp<float4>(c, L.stats_local);
-    } else {
+    if (p.world > 1) {
       for (int r = 0; r < p.world; ++r) {
         a.peer_stats.p[r] = c->symm[r] + L.stats[par];
         a.peer_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_STATS * kMaxRanks + p.rank;
@@ -592,12 +664,16 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.row_loss_local = row_loss;
     a.counter = counters + CNT_STATS;
     a.err = err;
-    const int grid = std::max(1, std::min<int>(cdiv(p.Bt, 8), p.sms));
-    PROFILED(K_STATS, s, ([&]() -> whale_status_t {
-               stats_combine_kernel<<<grid, 256, 0, s>>>(a);
-               CUDA_TRY(cudaGetLastError());
-               return WHALE_OK;
-             }()));
+    if (p.world == 1) {
+      // A4-A6 fused: lse, loss and G in one pass (no exchange needed)
+      const int64_t chunk = static_cast<int64_t>(kStatsThreads) * kGradVecs * (16 / ES);
+      PROFILED(K_STATS, s,
+               (launch(c, stats_grad_kernel<ES>, dim3(cdiv(p.Cr, chunk), p.Bt), dim3(kStatsThreads), 0, s, a,
+                       static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
+                       static_cast<float>(1.0 / static_cast<double>(p.Bt)))));
+    } else {
+      PROFILED(K_STATS, s, (launch(c, stats_rows_kernel<true>, dim3(p.Bt), dim3(kStatsThreads), 0, s, a)));
+    }
   }
   return WHALE_OK;
 }
@@ -622,11 +698,10 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
                                     cudaStream_t s) {
   const Plan& p = c->p;
   const Layout& L = p.L;
-  const int par = c->epoch & 1;
+  const int par = p.world == 1 ? 0 : (c->epoch & 1);
   unsigned* counters = wsp<unsigned>(c, L.counters);
   int* err = reinterpret_cast<int*>(counters + CNT_ERR);
-  const int32_t* yg = p.world == 1 ? wsp<int32_t>(c, L.yg_local)
-                                   : reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg[par]);
+  const int32_t* yg = p.world == 1 ? c->y_fwd : reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg[par]);
   {
     whale_status_t st = ensure_w_maps(c, w);
     if (st != WHALE_OK) return st;
@@ -636,93 +711,80 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     if (st != WHALE_OK) return st;
     c->dw_cached = dw;
   }
+  c->bwd_epoch += 1;
   // ---- A6 G = (softmax - onehot) / B_tot, in place over P~
-  {
+  if (p.world > 1) {  // (N = 1: already done by the forward's fused stats/grad kernel)
     constexpr int V = 16 / ES;
     dim3 grid(cdiv(cdiv(p.Cr, V), 256), static_cast<unsigned>(p.Bt));
-    PROFILED(K_GRAD, s, ([&]() -> whale_status_t {
-               softmax_grad_kernel<ES><<<grid, 256, 0, s>>>(c->ws + L.P, p.ldp, static_cast<int>(p.Bt), p.Cr,
-                                                            p.fwd.BN, p.fwd.n_blocks, wsp<float>(c, L.m_tile),
-                                                            wsp<float>(c, L.lse), yg, p.o_r,
-                                                            static_cast<float>(1.0 / static_cast<double>(p.Bt)));
-               CUDA_TRY(cudaGetLastError());
-               return WHALE_OK;
-             }()));
+    PROFILED(K_GRAD, s,
+             (launch(c, softmax_grad_kernel<ES>, grid, dim3(256), 0, s, static_cast<void*>(c->ws + L.P),
+                     static_cast<long long>(p.ldp), static_cast<int>(p.Bt), static_cast<long long>(p.Cr),
+                     p.fwd.BN, p.fwd.n_blocks, static_cast<const float*>(wsp<float>(c, L.m_tile)),
+                     static_cast<const float*>(wsp<float>(c, L.lse)), yg, static_cast<long long>(p.o_r),
+                     static_cast<float>(1.0 / static_cast<double>(p.Bt)))));
+  }
+  // ---- A8 args: fused split-K fixup; N = 1 writes dX, N > 1 pushes rows to their owners
+  GemmArgs ax = base_args(p.dx, static_cast<int>(p.Bt), static_cast<int>(p.D));
+  ax.err = err;
+  ax.part = wsp<float>(c, L.dxpart);
+  ax.st_out = wsp<float>(c, L.dxpart);
+  ax.tile_cnt = wsp<uint32_t>(c, L.tile_cnt);
+  ax.done_cnt = counters + CNT_DONE;
+  ax.epoch = c->bwd_epoch;
+  ax.B = static_cast<int>(p.B);
+  ax.rank = p.rank;
+  ax.world = p.world;
+  if (p.world == 1) {
+    ax.fix_mode = FIX_LOCAL;
+    ax.out = dx_local;
+  } else {
+    ax.fix_mode = FIX_PUSH;
+    for (int r = 0; r < p.world; ++r) {
+      ax.recv.p[r] = c->symm[r] + L.dxrecv[par];
+      ax.rs_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_RS * kMaxRanks + p.rank;
+    }
   }
   if constexpr (ES == 2) {
     // ---- A7 dW_r = G_r^T X  (A = G^T MN-major, B = X MN-major)
     {
       GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
       a.err = err;
+      a.st_out = static_cast<float*>(dw);
       PROFILED(K_DW, s,
                (launch_gemm<EPI_STORE_F32, true, true, 2>(c, 1, p.dw, c->tmG_dw, c->tmX_dw[par], c->tmDW, a, s)));
     }
-    // ---- A8 dX partials = G_r W_r  (A = G K-major, B = W_r MN-major), split-K
-    {
-      GemmArgs a = base_args(p.dx, static_cast<int>(p.Bt), static_cast<int>(p.D));
-      a.err = err;
-      PROFILED(K_DX, s,
-               (launch_gemm<EPI_STORE_F32, false, true, 2>(c, 2, p.dx, c->tmG_dx, c->tmW_dx, c->tmDxPart, a, s)));
-    }
+    // ---- A8 dX = G_r W_r  (A = G K-major, B = W_r MN-major), split-K + fused fixup
+    PROFILED(K_DX, s,
+             (launch_gemm<EPI_STORE_F32, false, true, 2>(c, 2, p.dx, c->tmG_dx, c->tmW_dx, c->tmDxPart, ax, s)));
   } else {
     // kind::tf32 accepts K-major operands only (plain 128B swizzle): transpose G, X, W_r.
-    const void* xg = p.world == 1 ? static_cast<const void*>(c->ws + L.xg_local)
-                                  : static_cast<const void*>(c->symm[p.rank] + L.xg[par]);
+    const void* xg = p.world == 1 ? c->x_fwd : static_cast<const void*>(c->symm[p.rank] + L.xg[par]);
     auto tr = [&](const void* src, long long sld, void* dst, long long dld, int64_t R, int64_t Cc) -> whale_status_t {
-      dim3 grid(cdiv(Cc, 32), cdiv(R, 32));
-      transpose_f32_kernel<<<grid, dim3(32, 32), 0, s>>>(static_cast<const float*>(src), sld,
-                                                         static_cast<float*>(dst), dld, static_cast<int>(R),
-                                                         static_cast<int>(Cc));
-      CUDA_TRY(cudaGetLastError());
-      return WHALE_OK;
+      return launch(c, transpose_f32_kernel, dim3(cdiv(Cc, 32), cdiv(R, 32)), dim3(32, 32), 0, s,
+                    static_cast<const float*>(src), sld, static_cast<float*>(dst), dld, static_cast<int>(R),
+                    static_cast<int>(Cc));
     };
-    PROFILED(K_GRAD, s, (tr(c->ws + L.P, p.ldp, c->ws + L.GT, L.ld_bt, p.Bt, p.Cr)));
-    PROFILED(K_GRAD, s, (tr(xg, p.D, c->ws + L.XT, L.ld_bt, p.Bt, p.D)));
-    PROFILED(K_GRAD, s, (tr(w, p.D, c->ws + L.WT, p.ldp, p.Cr, p.D)));
+    PROFILED(K_TRANSPOSE, s, (tr(c->ws + L.P, p.ldp, c->ws + L.GT, L.ld_bt, p.Bt, p.Cr)));
+    PROFILED(K_TRANSPOSE, s, (tr(xg, p.D, c->ws + L.XT, L.ld_bt, p.Bt, p.D)));
+    PROFILED(K_TRANSPOSE, s, (tr(w, p.D, c->ws + L.WT, p.ldp, p.Cr, p.D)));
     {
       GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
       a.err = err;
+      a.st_out = static_cast<float*>(dw);
       PROFILED(K_DW, s, (launch_gemm<EPI_STORE_F32, false, false, 4>(c, 4, p.dw, c->tmGT, c->tmXT, c->tmDW, a, s)));
     }
-    {
-      GemmArgs a = base_args(p.dx, static_cast<int>(p.Bt), static_cast<int>(p.D));
-      a.err = err;
-      PROFILED(K_DX, s,
-               (launch_gemm<EPI_STORE_F32, false, false, 4>(c, 5, p.dx, c->tmG_dx, c->tmWT, c->tmDxPart, a, s)));
-    }
+    PROFILED(K_DX, s,
+             (launch_gemm<EPI_STORE_F32, false, false, 4>(c, 5, p.dx, c->tmG_dx, c->tmWT, c->tmDxPart, ax, s)));
   }
-  // ---- A8 reduce-scatter to the DP owners
-  {
-    PeerPtrs recv{};
-    PeerFlags fl{};
-    if (p.world > 1) {
-      for (int r = 0; r < p.world; ++r) {
-        recv.p[r] = c->symm[r] + L.dxrecv[par];
-        fl.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_RS * kMaxRanks + p.rank;
-      }
-    }
-    const int64_t total = p.Bt * p.D / 4;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 2 * p.sms)));
-    PROFILED(K_RS_PUSH, s, ([&]() -> whale_status_t {
-               dx_push_kernel<ES><<<grid, 256, 0, s>>>(wsp<const float4>(c, L.dxpart), p.dx.splits,
-                                                       static_cast<int>(p.Bt), static_cast<int>(p.B),
-                                                       static_cast<int>(p.D), p.rank, p.world, recv, fl, c->epoch,
-                                                       dx_local, counters + CNT_RS);
-               CUDA_TRY(cudaGetLastError());
-               return WHALE_OK;
-             }()));
-    if (p.world > 1) {
-      const int64_t own = p.B * p.D / 4;
-      const int g2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(own, 256), 2 * p.sms)));
-      const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_RS * kMaxRanks;
-      PROFILED(K_RS_REDUCE, s, ([&]() -> whale_status_t {
-                 dx_reduce_kernel<ES><<<g2, 256, 0, s>>>(reinterpret_cast<const float4*>(recv.p[p.rank]),
-                                                         static_cast<int>(p.B), static_cast<int>(p.D), p.world,
-                                                         my_flags, c->epoch, dx_local, err);
-                 CUDA_TRY(cudaGetLastError());
-                 return WHALE_OK;
-               }()));
-    }
+  // ---- A8 owner side of the reduce-scatter (N > 1)
+  if (p.world > 1) {
+    const int64_t own = p.B * p.D / 4;
+    const int g2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(own, 256), 2 * p.sms)));
+    const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_RS * kMaxRanks;
+    PROFILED(K_RS_REDUCE, s,
+             (launch(c, dx_reduce_kernel<ES>, dim3(g2), dim3(256), 0, s,
+                     reinterpret_cast<const float4*>(c->symm[p.rank] + L.dxrecv[par]), static_cast<int>(p.B),
+                     static_cast<int>(p.D), p.world, my_flags, c->bwd_epoch, dx_local, err)));
   }
   return WHALE_OK;
 }
@@ -748,15 +810,16 @@ extern "C" whale_status_t whale_splitfc_check(whale_splitfc_ctx* ctx, void* stre
   CUDA_TRY(cudaMemcpy(&h, err, sizeof(int), cudaMemcpyDeviceToHost));
   if (h) CUDA_TRY(cudaMemset(err, 0, sizeof(int)));
   if (h & ERR_LABEL) return fail(WHALE_ERR_LABEL, "a label is outside [0, C)");
-  if (h & ERR_COMM) return fail(WHALE_ERR_COMM, "a peer flag wait timed out");
+  if (h & (ERR_COMM | 16)) return fail(WHALE_ERR_COMM, "a peer / split-K flag wait timed out");
   return WHALE_OK;
 }
 
 // ============================================================================ introspection
 extern "C" int32_t whale_splitfc_launches_per_step(const whale_splitfc_ctx* ctx) {
   if (!ctx) return 0;
-  const int extra = ctx->p.es == 4 ? 3 : 0;  // fp32 path: operand transposes
-  return (ctx->p.world == 1 ? 7 : 8) + extra;
+  // N = 1: logits, stats+grad, dW, dX;  N > 1: gather, logits, stats, grad, dW, dX, dX owner reduce
+  const int base = ctx->p.world == 1 ? 4 : 7;
+  return base + (ctx->p.es == 4 ? 3 : 0);  // fp32 path: operand transposes
 }
 
 extern "C" whale_status_t whale_splitfc_profile_enable(whale_splitfc_ctx* ctx, int32_t enable) {
@@ -801,20 +864,20 @@ extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, cha
   if (!ctx || !buf) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
   const Plan& p = ctx->p;
   auto g = [](const GemmCfg& c) {
-    char b[256];
+    char b[320];
     snprintf(b, sizeof(b),
-             "{\"BN\":%d,\"m_blocks\":%d,\"n_blocks\":%d,\"splits\":%d,\"num_kb\":%d,\"kb_per_split\":%d,"
-             "\"tiles\":%d,\"stages\":%d,\"smem\":%d,\"grid\":%d}",
-             c.BN, c.m_blocks, c.n_blocks, c.splits, c.num_kb, c.kb_per_split, c.num_tiles, c.stages, c.smem,
-             c.grid);
+             "{\"BN\":%d,\"bk\":%d,\"m_blocks\":%d,\"n_blocks\":%d,\"splits\":%d,\"num_kb\":%d,\"kb_per_split\":%d,"
+             "\"tiles\":%d,\"stages\":%d,\"epi_bufs\":%d,\"smem\":%d,\"grid\":%d}",
+             c.BN, c.bk, c.m_blocks, c.n_blocks, c.splits, c.num_kb, c.kb_per_split, c.num_tiles, c.stages, c.epi_bufs,
+             c.smem, c.grid);
     return std::string(b);
   };
-  char head[256];
+  char head[320];
   snprintf(head, sizeof(head),
            "{\"rank\":%d,\"world\":%d,\"B\":%lld,\"Bt\":%lld,\"D\":%lld,\"C\":%lld,\"C_r\":%lld,\"o_r\":%lld,"
-           "\"ldp\":%lld,\"sms\":%d,",
+           "\"ldp\":%lld,\"sms\":%d,\"es\":%d,\"pdl\":%d,",
            p.rank, p.world, (long long)p.B, (long long)p.Bt, (long long)p.D, (long long)p.C, (long long)p.Cr,
-           (long long)p.o_r, (long long)p.ldp, p.sms);
+           (long long)p.o_r, (long long)p.ldp, p.sms, p.es, ctx->pdl ? 1 : 0);
   std::string s = std::string(head) + "\"fwd\":" + g(p.fwd) + ",\"dw\":" + g(p.dw) + ",\"dx\":" + g(p.dx) +
                   ",\"off_P\":" + std::to_string(p.L.P) + ",\"off_m_tile\":" + std::to_string(p.L.m_tile) +
                   ",\"off_s_tile\":" + std::to_string(p.L.s_tile) + ",\"off_lse\":" + std::to_string(p.L.lse) +
