@@ -138,6 +138,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of one CUDA graph per step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -176,7 +177,16 @@ def main():
     es = 2 if cfg.dtype == "bf16" else 4
     w_bytes = C_r * cfg.D * es
     flush_l2 = w_bytes < 2 * L2_BYTES
-    flush_buf = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev) if flush_l2 else None
+    flush_bufs = None
+    if flush_l2:
+        flush_bufs = (torch.empty(64 * 2 ** 20, dtype=torch.float32, device=dev),
+                      torch.ones(64 * 2 ** 20, dtype=torch.float32, device=dev))
+
+    def flush():
+        # write 256 MiB (> L2), then read another 256 MiB: the read evicts the written dirty
+        # lines too, so their write-back happens here and not inside the next timed step
+        flush_bufs[0].zero_()
+        flush_bufs[1].sum()
 
     def step():
         op.forward(X, y, W)
@@ -191,6 +201,17 @@ def main():
         step()
     op.check()
     torch.cuda.synchronize()
+    # one CUDA graph per step (the library keeps its step epoch on the device, so replays
+    # are valid collective steps); falls back to eager launches with --no-graph
+    run = step
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+        op.check()
+        run = graph.replay
 
     # ---------------- timed region (device time, CUDA events on the launching stream)
     clocks = ClockSampler(local_rank)
@@ -201,9 +222,9 @@ def main():
     if flush_l2:
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for a, b in evs:
-            flush_buf.zero_()  # > L2: evicts the previous step's working set (outside the events)
+            flush()  # > L2: evicts the previous step's working set (outside the events)
             a.record(s)
-            step()
+            run()
             b.record(s)
         torch.cuda.synchronize()
         total_ms = sum(a.elapsed_time(b) for a, b in evs)
@@ -211,7 +232,7 @@ def main():
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
         for _ in range(args.steps):
-            step()
+            run()
         b.record(s)
         torch.cuda.synchronize()
         total_ms = a.elapsed_time(b)
@@ -231,7 +252,7 @@ def main():
     op.profile(True)
     for _ in range(args.steps):
         if flush_l2:
-            flush_buf.zero_()
+            flush()
         step()
     torch.cuda.synchronize()
     kern = op.profile_read()
@@ -254,11 +275,19 @@ def main():
     for _ in range(3):
         e2e_step()
     torch.cuda.synchronize()
+    run_e2e = e2e_step
+    if not args.no_graph:
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            e2e_step()
+        g2.replay()
+        torch.cuda.synchronize()
+        run_e2e = g2.replay
     barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(s)
     for _ in range(args.steps):
-        e2e_step()
+        run_e2e()
     b.record(s)
     torch.cuda.synchronize()
     barrier()
@@ -294,9 +323,11 @@ def main():
         "config": {
             "workload": workload_desc(args.config, cfg, world), "D": cfg.D, "C": cfg.C, "B_per_gpu": cfg.B,
             "global_batch": Bt, "C_shard_rank0": cfgj["C_r"], "parallelism": f"dp{world}-backbone/mp{world}-fc",
-            "l2": ("flushed between timed steps (256 MiB write, outside the step events)" if flush_l2
+            "l2": ("flushed between timed steps outside the step events (256 MiB write + 256 MiB read, so no "
+                   "dirty flush lines are written back inside a step)" if flush_l2
                    else f"inputs larger than L2 (W shard {w_bytes / 2 ** 20:.0f} MiB > 2x126 MiB)"),
             "tiles": {k: cfgj[k] for k in ("fwd", "dw", "dx")},
+            "launch": "eager" if args.no_graph else "CUDA graph per step (PDL edges)",
         },
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": X.numel() * X.element_size() + y.numel() * 4,
@@ -327,6 +358,10 @@ def kernel_work(name, cfgj, cfg, es):
         return Bt * Cr * es + Bt * D * es + Cr * D * 4, 2 * Bt * Cr * D
     if name == "dx_gemm":       # read G, W_r; write split-K partials
         return Bt * Cr * es + Cr * D * es + S * Bt * D * 4, 2 * Bt * Cr * D
+    if name == "bwd_gemm":      # fused dX (read G, W_r; partials) + dW (read G, X; write dW)
+        bx, fx = kernel_work("dx_gemm", cfgj, cfg, es)
+        bw, fw = kernel_work("dw_gemm", cfgj, cfg, es)
+        return bx + bw, fx + fw
     if name == "softmax_grad":  # read + write P~/G in place, read tile maxima
         return 2 * Bt * Cr * es + Bt * T * 4, 0
     if name == "stats_combine":

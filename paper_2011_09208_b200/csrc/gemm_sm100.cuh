@@ -68,13 +68,16 @@ struct GemmArgs {
   // producer-side wait for peer data (NVLink all-gather) before the first A load
   const uint32_t* wait_flags;  // [wait_count] local flag words, NULL = no wait
   int wait_count;
-  uint32_t wait_epoch;
+  uint32_t wait_mult;       // wait until flag >= epoch * wait_mult (monotonic counters)
+  // step epoch: every kernel reads e = *dev_epoch + 1 (device-resident, so a whole step can
+  // be captured once in a CUDA graph and replayed); the last backward kernel bumps it
+  uint32_t* dev_epoch;
+  int bump_epoch;           // 1: this launch ends the step (end ticket -> RS signal, epoch++)
   // split-K fixup (EPI_STORE_F32, dX)
   int fix_mode;             // FixMode
   const float* part;        // [splits x M x N] fp32 partials (the tmOut tensor)
   uint32_t* tile_cnt;       // [m_blocks x n_blocks] monotonic arrival counters
-  uint32_t* done_cnt;       // monotonic count of reduced tile shares
-  uint32_t epoch;           // launch epoch (counters reach epoch * splits)
+  uint32_t* done_cnt;       // monotonic end-of-kernel ticket (CTAs)
   void* out;                // FIX_LOCAL: final dX [M x N] (ES-sized elements)
   int B, rank, world;       // FIX_PUSH: rows r*B..(r+1)*B belong to rank r
   PeerPtrs recv;            // FIX_PUSH: owner's fp32 slab [world][B x N] (this parity)
@@ -167,6 +170,24 @@ __device__ __forceinline__ void fixup_share(const GemmArgs& a, int mb, int nb, i
   }
 }
 
+// End of the backward's last GEMM launch (after the CTA-wide __syncthreads): the last CTA
+// to finish raises flag[RS] = e on every rank (N > 1: all of this rank's dX pushes have
+// landed AND every CTA finished reading the gathered X, so peers may overwrite it next
+// step) and publishes the step epoch for the following kernels.
+__device__ __forceinline__ void end_of_step_ticket(const GemmArgs& a, uint32_t e, int& s_last) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t done = atomicAdd(a.done_cnt, 1u) + 1u;
+    s_last = (done == e * gridDim.x);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence_system();
+  if (threadIdx.x < a.world && a.fix_mode == FIX_PUSH) st_relaxed_sys(a.rs_flags.p[threadIdx.x], e);  // fenced above
+  __syncthreads();
+  if (threadIdx.x == 0) atomicExch(a.dev_epoch, e);
+}
+
 // ES = operand element size: 2 -> bf16 (kind::f16), 4 -> fp32 storage run as kind::tf32.
 template <int EPI, bool A_MN, bool B_MN, int ES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -211,6 +232,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
   pdl_wait();      // everything below reads/writes memory the previous kernel may touch
   pdl_trigger();
+  TraceScope _trace(EPI == EPI_FWD_STATS ? 1 : (a.fix_mode != FIX_NONE ? 5 : 4));
+  const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;  // this step's epoch
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -218,7 +241,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (a.wait_flags != nullptr) {
         // peers' rows of A were pushed over NVLink by generic-proxy stores; acquire their
         // flags, then order the async-proxy (TMA) reads after them.
-        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, a.wait_epoch, a.err, 8);
+        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, 8);
         fence_proxy_async_global();
       }
       int stage = 0;
@@ -481,7 +504,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t* cnt = a.tile_cnt + mb * a.n_blocks + nb;
           if (threadIdx.x == 128) {
             atomicAdd(cnt, 1u);
-            const uint32_t target = a.epoch * static_cast<uint32_t>(a.splits);
+            const uint32_t target = e * static_cast<uint32_t>(a.splits);
             if (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0) {
               SpinGuard g;
               while (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0) g.check(a.err, 16);
@@ -490,19 +513,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           named_bar_sync(1, 128);
           __threadfence();
           fixup_share<ES>(a, mb, nb, sp, threadIdx.x - 128);
-          if (a.fix_mode == FIX_PUSH) {
-            __threadfence_system();
-            named_bar_sync(1, 128);
-            if (threadIdx.x == 128) {
-              const uint32_t done = atomicAdd(a.done_cnt, 1u) + 1u;
-              s_fix_go = (done == a.epoch * static_cast<uint32_t>(a.num_tiles));
-            }
-            named_bar_sync(1, 128);
-            if (s_fix_go) {  // every share of every tile is in its owner's slab: signal
-              __threadfence_system();
-              if (threadIdx.x - 128 < a.world) st_release_sys(a.rs_flags.p[threadIdx.x - 128], a.epoch);
-            }
-          }
         }
       }
     }
@@ -514,6 +524,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
   }
+  if (a.bump_epoch) end_of_step_ticket(a, e, s_fix_go);
 }
 
 }  // namespace whale

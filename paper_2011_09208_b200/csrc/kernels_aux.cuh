@@ -22,6 +22,14 @@ namespace whale {
 
 enum ErrBits : int { ERR_LABEL = 1, ERR_COMM = 8 };
 
+// debug timestamps (globaltimer ns) for latency experiments; read via whale_debug_timestamps
+__device__ unsigned long long g_dbg_ts[32];
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Last-block-done ticket: true in exactly one (the last) block, after all blocks' prior
 // global writes are visible at `sys` (cross-GPU) or gpu scope.
 template <bool kSys>
@@ -31,7 +39,7 @@ __device__ __forceinline__ bool last_block_ticket(unsigned* counter) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned t = atomicAdd(counter, 1u);
-    is_last = (t == gridDim.x - 1);
+    is_last = (t == gridDim.x * gridDim.y * gridDim.z - 1);
   }
   __syncthreads();
   if (is_last) {
@@ -47,16 +55,21 @@ __global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const in
                                      int64_t x_vecs /*B*row_bytes/16*/, int B, int rank, int world,
                                      PeerPtrs dst_x /*slab base on each rank*/, PeerPtrs dst_y,
                                      PeerFlags flags /*&flag[GATHER][rank] on each rank*/, uint32_t epoch,
-                                     unsigned* counter) {
-  pdl_wait();
+                                     int dbg) {
+  const bool ts = (dbg & 16) && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1);
+  const int tso = blockIdx.x == 0 ? 0 : 8;
+  if (ts) g_dbg_ts[tso + 0] = globaltimer();
+  if (!(dbg & 4)) pdl_wait();
   pdl_trigger();
+  TraceScope _trace(0);
+  if (ts) g_dbg_ts[tso + 1] = globaltimer();
   const int64_t off_vec = static_cast<int64_t>(rank) * x_vecs;
   for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < x_vecs;
        v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint4 val = __ldg(x_local + v);
 #pragma unroll
     for (int p = 0; p < kMaxRanks; ++p)
-      if (p < world) reinterpret_cast<uint4*>(dst_x.p[p])[off_vec + v] = val;
+      if (p < world && (!(dbg & 1) || p == rank)) reinterpret_cast<uint4*>(dst_x.p[p])[off_vec + v] = val;
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x) {
     const int32_t y = y_local[i];
@@ -64,10 +77,17 @@ __global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const in
     for (int p = 0; p < kMaxRanks; ++p)
       if (p < world) reinterpret_cast<int32_t*>(dst_y.p[p])[rank * B + i] = y;
   }
-  if (last_block_ticket<true>(counter)) {
-    if (threadIdx.x < world) st_release_sys(flags.p[threadIdx.x], epoch);
-    __syncthreads();
-    if (threadIdx.x == 0) *counter = 0;
+  // every block signals every peer itself (no last-block ticket): after the CTA barrier,
+  // one fence.sc.sys + a release increment per peer; peers wait for epoch * gridDim.x.
+  (void)epoch;
+  if (ts) g_dbg_ts[tso + 2] = globaltimer();
+  __syncthreads();
+  if (ts) g_dbg_ts[tso + 3] = globaltimer();
+  if (threadIdx.x == 0) {
+    if (!(dbg & 2)) __threadfence_system();
+    if (ts) g_dbg_ts[tso + 4] = globaltimer();
+    for (int p = 0; p < world; ++p) red_add_relaxed_sys(flags.p[p], 1u);  // ordered by the fence
+    if (ts) g_dbg_ts[tso + 5] = globaltimer();
   }
 }
 
@@ -82,7 +102,7 @@ struct StatsArgs {
   PeerPtrs peer_stats;   // float4 [world x Bt] slab on each rank (this parity)
   PeerFlags peer_flags;  // &flag[STATS][rank] on each rank
   const uint32_t* my_flags;  // flag[STATS][0..world) on this rank
-  uint32_t epoch;
+  const uint32_t* dev_epoch; // step epoch e = *dev_epoch + 1 (device-resident, graph-capturable)
   float4* my_stats;      // this rank's slab (N > 1)
   float* lse;            // [Bt]
   float* row_loss_all;   // [Bt]
@@ -118,6 +138,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_rows_kernel(const StatsAr
   __shared__ float red[4];
   pdl_wait();
   pdl_trigger();
+  TraceScope _trace(2);
   const int i = blockIdx.x;
   const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
   const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
@@ -156,8 +177,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_rows_kernel(const StatsAr
   if (!last_block_ticket<kMulti>(a.counter)) return;
   // ---- last CTA: (N > 1) exchange + rank-ordered combine; fixed-order mean loss ----
   if constexpr (kMulti) {
-    if (threadIdx.x < a.world) st_release_sys(a.peer_flags.p[threadIdx.x], a.epoch);
-    if (threadIdx.x < a.world) wait_flag_geq(a.my_flags + threadIdx.x, a.epoch, a.err, ERR_COMM);
+    const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;
+    if (threadIdx.x < a.world) st_release_sys(a.peer_flags.p[threadIdx.x], e);
+    if (threadIdx.x < a.world) wait_flag_geq(a.my_flags + threadIdx.x, e, a.err, ERR_COMM);
     __syncthreads();
     __threadfence_system();
     for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) {
@@ -200,6 +222,7 @@ __global__ void __launch_bounds__(256) softmax_grad_kernel(void* P, long long ld
   constexpr int V = 16 / ES;
   pdl_wait();
   pdl_trigger();
+  TraceScope _trace(3);
   const int i = blockIdx.y;
   const long long j0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * V;
   if (j0 >= C_r) return;
@@ -246,6 +269,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
   __shared__ float red[4];
   pdl_wait();
   pdl_trigger();
+  TraceScope _trace(2);
   const int i = blockIdx.y;
   const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
   const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
@@ -320,16 +344,135 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
   }
 }
 
+// ---------------------------------------------------------------- A4-A6 fused (N > 1)
+// grid (B_tot rows, chunks): x = row so every row's chunk-0 CTA is dispatched first.
+// Each CTA reduces its row's local class tiles to (m_r, s_r); the chunk-0 CTA also takes
+// z_y,r and pushes the float4 record into every peer's slab [rank][row] followed by a
+// per-row release flag.  Every CTA of the row then acquires the world flags of its row,
+// combines the records in rank order (identical bits on every rank and every chunk CTA),
+// and turns its chunk of P~ into G.  Chunk 0 writes lse / row loss; the last CTA (local
+// ticket) sums the mean loss in a fixed order.
+template <int ES>
+__global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const StatsArgs a, void* P, long long ldp,
+                                                                         int BN, float inv_bt,
+                                                                         PeerFlags row_flags /*peer p: &rf[rank*Bt]*/,
+                                                                         const uint32_t* my_row_flags /*[world*Bt]*/) {
+  constexpr int V = 16 / ES;
+  __shared__ float red[4];
+  __shared__ float4 recs[kMaxRanks];
+  pdl_wait();
+  pdl_trigger();
+  TraceScope _trace(2);
+  const int i = blockIdx.x;
+  const int chunk_id = blockIdx.y;
+  const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;
+  const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
+  const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
+  const long long y = a.y[i];
+  const long long yl = y - a.o_r;
+  if (chunk_id == 0) {
+    float mloc[8], sloc[8];
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = threadIdx.x + k * kStatsThreads;
+      mloc[k] = t < a.T ? __ldg(mt + t) : -INFINITY;
+      sloc[k] = t < a.T ? __ldg(st + t) : 0.f;
+      m = fmaxf(m, mloc[k]);
+    }
+    for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, __ldg(mt + t));
+    m = block_max128(m, red);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += sloc[k] * __expf(mloc[k] - m);
+    for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads)
+      s += __ldg(st + t) * __expf(__ldg(mt + t) - m);
+    s = block_sum128(s, red);
+    if (threadIdx.x < a.world) {  // thread p pushes the record + flag to peer p
+      if (threadIdx.x == 0 && (y < 0 || y >= a.C)) atomicOr(a.err, ERR_LABEL);
+      const bool own = (y >= a.o_r) && (y < a.o_r + a.C_r);
+      const float zy = own ? a.zy_r[i] : 0.f;
+      const int p = threadIdx.x;
+      reinterpret_cast<float4*>(a.peer_stats.p[p])[static_cast<size_t>(a.rank) * a.Bt + i] = make_float4(m, s, zy, 0.f);
+      __threadfence_system();  // record before flag (fence + relaxed: cheaper than a release store)
+      st_relaxed_sys(row_flags.p[p] + i, e);
+    }
+  }
+  // ---- acquire the row's records from every rank, combine in rank order
+  if (threadIdx.x < a.world) {
+    wait_flag_geq(my_row_flags + static_cast<size_t>(threadIdx.x) * a.Bt + i, e, a.err, ERR_COMM);
+    recs[threadIdx.x] = __ldcg(a.my_stats + static_cast<size_t>(threadIdx.x) * a.Bt + i);
+  }
+  __syncthreads();
+  float mm = -INFINITY;
+  for (int p = 0; p < a.world; ++p) mm = fmaxf(mm, recs[p].x);
+  float ss = 0.f, zz = 0.f;
+  for (int p = 0; p < a.world; ++p) {
+    ss += recs[p].y * __expf(recs[p].x - mm);
+    zz += recs[p].z;  // exactly one rank owns the label; the others contribute 0
+  }
+  const float l = mm + logf(ss);
+  if (chunk_id == 0 && threadIdx.x == 0) {
+    a.lse[i] = l;
+    a.row_loss_all[i] = l - zz;
+    if (a.row_loss_local && i >= a.rank * a.B && i < (a.rank + 1) * a.B) a.row_loss_local[i - a.rank * a.B] = l - zz;
+  }
+  // ---- G for this CTA's chunk of the row
+  const long long chunk = static_cast<long long>(kStatsThreads) * kGradVecs * V;
+#pragma unroll
+  for (int k = 0; k < kGradVecs; ++k) {
+    const long long j0 = chunk_id * chunk + (static_cast<long long>(k) * kStatsThreads + threadIdx.x) * V;
+    if (j0 >= a.C_r) break;
+    const float scale = __expf(__ldg(mt + j0 / BN) - l) * inv_bt;
+    if constexpr (ES == 2) {
+      uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P) + i * ldp + j0);
+      uint4 raw = *p;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float2 f = __bfloat1622float2(h[q]);
+        const long long j = j0 + 2 * q;
+        f.x = f.x * scale - ((j == yl) ? inv_bt : 0.f);
+        f.y = f.y * scale - ((j + 1 == yl) ? inv_bt : 0.f);
+        h[q] = __floats2bfloat162_rn(f.x, f.y);
+      }
+      *p = raw;
+    } else {
+      float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(P) + i * ldp + j0);
+      float4 f = *p;
+      f.x = f.x * scale - ((j0 == yl) ? inv_bt : 0.f);
+      f.y = f.y * scale - ((j0 + 1 == yl) ? inv_bt : 0.f);
+      f.z = f.z * scale - ((j0 + 2 == yl) ? inv_bt : 0.f);
+      f.w = f.w * scale - ((j0 + 3 == yl) ? inv_bt : 0.f);
+      *p = f;
+    }
+  }
+  if (!last_block_ticket<false>(a.counter)) return;
+  double acc = 0.0;
+  for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) acc += static_cast<double>(__ldcg(a.row_loss_all + r));
+  __shared__ double part[4];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *a.loss = static_cast<float>(((part[0] + part[1]) + (part[2] + part[3])) / a.Bt);
+    *a.counter = 0;
+  }
+}
+
 // ---------------------------------------------------------------- A8 dX reduce-scatter (owner)
 // The dX GEMM's fixup pushed every peer's reduced rows into recv[p][B x D] and raised
 // flag[RS][p]; wait for all, then dX_r = sum_p recv[p] in rank order.
 template <int ES>
 __global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict__ recv, int B, int D, int world,
-                                                        const uint32_t* my_flags, uint32_t epoch, void* dx_local,
-                                                        int* err) {
+                                                        const uint32_t* my_flags, const uint32_t* dev_epoch,
+                                                        void* dx_local, int* err) {
   pdl_wait();
   pdl_trigger();
-  if (threadIdx.x < world) wait_flag_geq(my_flags + threadIdx.x, epoch, err, ERR_COMM);
+  TraceScope _trace(6);
+  // the backward GEMM already published this step's epoch (end-of-step ticket)
+  const uint32_t e = ld_acquire_gpu(dev_epoch);
+  if (threadIdx.x < world) wait_flag_geq(my_flags + threadIdx.x, e, err, ERR_COMM);
   __syncthreads();
   __threadfence_system();
   const int64_t total = static_cast<int64_t>(B) * (D / 4);
@@ -352,6 +495,14 @@ __global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict
   }
 }
 
+// Forward-only steps (a forward not followed by a backward) end here: publish the epoch.
+__global__ void epoch_bump_kernel(uint32_t* dev_epoch) {
+  pdl_wait();
+  pdl_trigger();
+  TraceScope _trace(9);
+  if (threadIdx.x == 0) atomicAdd(dev_epoch, 1u);
+}
+
 // ---------------------------------------------------------------- fp32 operand transposes
 // kind::tf32 takes only K-major smem operands in the plain 128B swizzle, so the fp32
 // (tiny) backward feeds dW / dX from transposed copies: dst[c, r] = src[r, c].
@@ -361,6 +512,7 @@ __global__ void __launch_bounds__(1024) transpose_f32_kernel(const float* __rest
   __shared__ float t[32][33];
   pdl_wait();
   pdl_trigger();
+  TraceScope _trace(7);
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
   if (r0 + ty < R && c0 + tx < Cc) t[ty][tx] = src[(r0 + ty) * src_ld + c0 + tx];

@@ -13,6 +13,7 @@
 
 #include "../../include/whale_splitfc.h"
 #include "gemm_sm100.cuh"
+#include "bwd_sm100.cuh"
 #include "kernels_aux.cuh"
 
 using namespace whale;
@@ -95,11 +96,13 @@ struct Layout {
   size_t XT = 0, GT = 0, WT = 0;
   int64_t ld_bt = 0;
   // symmetric buffer offsets (per parity for the slabs); world > 1 only
-  size_t flags = 0, xg[2] = {0, 0}, yg[2] = {0, 0}, stats[2] = {0, 0}, dxrecv[2] = {0, 0}, symm_total = 0;
+  // single-buffered: a rank overwrites a peer's slab only after that peer's end-of-step
+  // ticket (RS flag) proved it finished reading it (see end_of_step_ticket)
+  size_t flags = 0, rowflags = 0, xg = 0, yg = 0, stats = 0, dxrecv = 0, symm_total = 0;
 };
 
 enum FlagKind { FLAG_GATHER = 0, FLAG_STATS = 1, FLAG_RS = 2 };
-enum CounterIdx { CNT_GATHER = 0, CNT_STATS = 1, CNT_DONE = 2, CNT_ERR = 16 };
+enum CounterIdx { CNT_GATHER = 0, CNT_STATS = 1, CNT_DONE = 2, CNT_SCHED = 3, CNT_EPOCH = 4, CNT_ERR = 16 };
 
 struct Plan {
   int rank = 0, world = 1, es = 2;
@@ -268,12 +271,11 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   o = 0;
   if (p.world > 1) {
     L.flags = take(4 * kMaxRanks * 4);
-    for (int par = 0; par < 2; ++par) {
-      L.xg[par] = take(static_cast<size_t>(p.Bt) * p.D * p.es);
-      L.yg[par] = take(p.Bt * 4);
-      L.stats[par] = take(static_cast<size_t>(p.world) * p.Bt * 16);
-      L.dxrecv[par] = take(static_cast<size_t>(p.world) * p.B * p.D * 4);
-    }
+    L.rowflags = take(static_cast<size_t>(p.world) * p.Bt * 4);
+    L.xg = take(static_cast<size_t>(p.Bt) * p.D * p.es);
+    L.yg = take(p.Bt * 4);
+    L.stats = take(static_cast<size_t>(p.world) * p.Bt * 16);
+    L.dxrecv = take(static_cast<size_t>(p.world) * p.B * p.D * 4);
   }
   L.symm_total = o;
   return WHALE_OK;
@@ -357,16 +359,16 @@ struct ProfRec {
   int kind;
   cudaEvent_t a, b;
 };
-static const char* kKindNames[] = {"bridge_gather", "logits_gemm", "stats_combine", "softmax_grad",
-                                   "dw_gemm",       "dx_gemm",     "dx_rs_reduce",  "transpose_f32"};
-enum KernelKind { K_GATHER, K_LOGITS, K_STATS, K_GRAD, K_DW, K_DX, K_RS_REDUCE, K_TRANSPOSE, K_NUM };
+static const char* kKindNames[] = {"bridge_gather", "logits_gemm",  "stats_combine", "softmax_grad", "dw_gemm",
+                                   "dx_gemm",       "dx_rs_reduce", "transpose_f32", "bwd_gemm"};
+enum KernelKind { K_GATHER, K_LOGITS, K_STATS, K_GRAD, K_DW, K_DX, K_RS_REDUCE, K_TRANSPOSE, K_BWD, K_NUM };
 
 struct whale_splitfc_ctx {
   Plan p;
   uint8_t* ws = nullptr;
   uint8_t* symm[kMaxRanks] = {};
   // static maps (X maps: per parity at N > 1; cached on the caller's X at N = 1)
-  CUtensorMap tmX_fwd[2], tmX_dw[2], tmP_store, tmG_dx, tmG_dw, tmDxPart;
+  CUtensorMap tmX_fwd, tmX_dw, tmP_store, tmG_dx, tmG_dw, tmDxPart;
   CUtensorMap tmGT, tmXT, tmWT;  // fp32 path: K-major transposed operands
   // pointer-cached maps
   const void* x_cached = nullptr;
@@ -380,6 +382,8 @@ struct whale_splitfc_ctx {
   uint32_t bwd_epoch = 0;            // backward count (fixup counters)
   bool have_fwd = false;
   bool pdl = true;
+  bool fused_bwd = true;             // dW + dX in one persistent launch (bf16)
+  int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
   std::vector<ProfRec> prof;
   double prof_ms[K_NUM] = {};
@@ -515,13 +519,22 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   }
   const char* pdl_env = getenv("WHALE_PDL");
   c->pdl = !(pdl_env && pdl_env[0] == '0');
+  c->fused_bwd = p.es == 2 && env_int("WHALE_FUSED_BWD", 1) != 0 && g_store_mode == 1;
+  if (c->fused_bwd) {
+    c->bwd_stage_bytes = std::max(p.dx.stage_bytes, p.dw.stage_bytes);
+    c->bwd_epi_bufs = 4;  // CTA-wide 16 KB store stages
+    const int fixed = 1024 + 512 + c->bwd_epi_bufs * 4 * kEpiBufBytes;
+    c->bwd_stages = std::min(8, (kSmemLimit - kStaticSmemSlack - fixed) / c->bwd_stage_bytes);
+    c->bwd_smem = fixed + c->bwd_stages * c->bwd_stage_bytes;
+    if (c->bwd_stages < 2) c->fused_bwd = false;
+  }
   // static TMA maps
   const int es = p.es, kbk = kRowBytes / es, atom = kRowBytes / es;
   if (p.world > 1) {
-    for (int par = 0; par < 2; ++par) {
-      const void* xg = c->symm[p.rank] + p.L.xg[par];
-      MAP_TRY(map2d(&c->tmX_fwd[par], xg, es, p.D, p.Bt, p.D * es, kbk, kBM));
-      MAP_TRY(map2d(&c->tmX_dw[par], xg, es, p.D, p.Bt, p.D * es, atom, p.dw.bk));
+    {
+      const void* xg = c->symm[p.rank] + p.L.xg;
+      MAP_TRY(map2d(&c->tmX_fwd, xg, es, p.D, p.Bt, p.D * es, kbk, kBM));
+      MAP_TRY(map2d(&c->tmX_dw, xg, es, p.D, p.Bt, p.D * es, atom, p.dw.bk));
     }
   }
   void* P = c->ws + p.L.P;
@@ -571,12 +584,19 @@ static whale_status_t ensure_x_maps(whale_splitfc_ctx* c, const void* x) {
   if (x == c->x_cached) return WHALE_OK;
   const Plan& p = c->p;
   const int kbk = kRowBytes / p.es, atom = kRowBytes / p.es;
-  whale_status_t st = map2d(&c->tmX_fwd[0], x, p.es, p.D, p.Bt, p.D * p.es, kbk, kBM);
+  whale_status_t st = map2d(&c->tmX_fwd, x, p.es, p.D, p.Bt, p.D * p.es, kbk, kBM);
   if (st != WHALE_OK) return st;
-  st = map2d(&c->tmX_dw[0], x, p.es, p.D, p.Bt, p.D * p.es, atom, p.dw.bk);
+  st = map2d(&c->tmX_dw, x, p.es, p.D, p.Bt, p.D * p.es, atom, p.dw.bk);
   if (st != WHALE_OK) return st;
   c->x_cached = x;
   return WHALE_OK;
+}
+
+// Blocks of the bridge gather: identical on every rank (depends on B, D only); each block
+// raises the peers' GATHER counters once, so the consumer waits for epoch * grid.
+static int gather_grid(const Plan& p) {
+  const int64_t x_vecs = p.B * p.D * p.es / 16;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(x_vecs, 256), 64)));
 }
 
 // ============================================================================ forward
@@ -585,9 +605,9 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
                                    const void* w, float* loss, float* row_loss, cudaStream_t s) {
   const Plan& p = c->p;
   const Layout& L = p.L;
-  const int par = p.world == 1 ? 0 : (c->epoch & 1);
   unsigned* counters = wsp<unsigned>(c, L.counters);
   int* err = reinterpret_cast<int*>(counters + CNT_ERR);
+  uint32_t* dev_epoch = counters + CNT_EPOCH;
   {
     whale_status_t st = ensure_w_maps(c, w);
     if (st != WHALE_OK) return st;
@@ -604,21 +624,22 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     PeerPtrs dx{}, dy{};
     PeerFlags fl{};
     for (int r = 0; r < p.world; ++r) {
-      dx.p[r] = c->symm[r] + L.xg[par];
-      dy.p[r] = c->symm[r] + L.yg[par];
+      dx.p[r] = c->symm[r] + L.xg;
+      dy.p[r] = c->symm[r] + L.yg;
       fl.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_GATHER * kMaxRanks + p.rank;
     }
-    yg = reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg[par]);
+    yg = reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg);
     const int64_t x_vecs = p.B * p.D * ES / 16;
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(x_vecs, 256), 2 * p.sms)));
+    const int grid = gather_grid(p);
     PROFILED(K_GATHER, s,
              (launch(c, bridge_gather_kernel, dim3(grid), dim3(256), 0, s, static_cast<const uint4*>(x_local),
-                     y_local, x_vecs, static_cast<int>(p.B), p.rank, p.world, dx, dy, fl, c->epoch,
-                     counters + CNT_GATHER)));
+                     y_local, x_vecs, static_cast<int>(p.B), p.rank, p.world, dx, dy, fl, 0u,
+                     env_int("WHALE_GATHER_DBG", 0))));
   }
   // ---- A3 logits GEMM with fused row statistics
   {
     GemmArgs a = base_args(p.fwd, static_cast<int>(p.Bt), static_cast<int>(p.Cr));
+    a.dev_epoch = dev_epoch;
     a.labels = yg;
     a.class_offset = p.o_r;
     a.m_tile = wsp<float>(c, L.m_tile);
@@ -628,10 +649,10 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     if (p.world > 1) {
       a.wait_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_GATHER * kMaxRanks;
       a.wait_count = p.world;
-      a.wait_epoch = c->epoch;
+      a.wait_mult = static_cast<uint32_t>(gather_grid(p));  // one increment per gather block
     }
     PROFILED(K_LOGITS, s,
-             (launch_gemm<EPI_FWD_STATS, false, false, ES>(c, ES == 2 ? 0 : 3, p.fwd, c->tmX_fwd[par],
+             (launch_gemm<EPI_FWD_STATS, false, false, ES>(c, ES == 2 ? 0 : 3, p.fwd, c->tmX_fwd,
                                                            c->tmW_fwd, c->tmP_store, a, s)));
   }
   // ---- A4 + A5 statistics (exchange), combine, loss
@@ -651,13 +672,13 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.C = p.C;
     if (p.world > 1) {
       for (int r = 0; r < p.world; ++r) {
-        a.peer_stats.p[r] = c->symm[r] + L.stats[par];
+        a.peer_stats.p[r] = c->symm[r] + L.stats;
         a.peer_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_STATS * kMaxRanks + p.rank;
       }
       a.my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_STATS * kMaxRanks;
-      a.my_stats = reinterpret_cast<float4*>(c->symm[p.rank] + L.stats[par]);
+      a.my_stats = reinterpret_cast<float4*>(c->symm[p.rank] + L.stats);
     }
-    a.epoch = c->epoch;
+    a.dev_epoch = dev_epoch;
     a.lse = wsp<float>(c, L.lse);
     a.row_loss_all = wsp<float>(c, L.row_loss);
     a.loss = loss;
@@ -672,7 +693,16 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
                        static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
                        static_cast<float>(1.0 / static_cast<double>(p.Bt)))));
     } else {
-      PROFILED(K_STATS, s, (launch(c, stats_rows_kernel<true>, dim3(p.Bt), dim3(kStatsThreads), 0, s, a)));
+      // A4-A6 fused with the per-row cross-GPU exchange (chunk-0 CTAs of every row first)
+      PeerFlags rf{};
+      for (int r = 0; r < p.world; ++r)
+        rf.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.rowflags) + static_cast<size_t>(p.rank) * p.Bt;
+      const int64_t chunk = static_cast<int64_t>(kStatsThreads) * kGradVecs * (16 / ES);
+      PROFILED(K_STATS, s,
+               (launch(c, stats_grad_multi_kernel<ES>, dim3(p.Bt, cdiv(p.Cr, chunk)), dim3(kStatsThreads), 0, s, a,
+                       static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
+                       static_cast<float>(1.0 / static_cast<double>(p.Bt)), rf,
+                       reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.rowflags))));
     }
   }
   return WHALE_OK;
@@ -686,6 +716,12 @@ extern "C" whale_status_t whale_splitfc_forward(whale_splitfc_ctx* ctx, const vo
     return fail(WHALE_ERR_INVALID_ARG, "x_local / w_shard must be 16-byte aligned");
   ctx->epoch += 1;
   auto s = static_cast<cudaStream_t>(stream);
+  if (ctx->have_fwd) {
+    // the previous forward had no backward (forward-only step): end that step's epoch
+    uint32_t* dev_epoch = wsp<unsigned>(ctx, ctx->p.L.counters) + CNT_EPOCH;
+    whale_status_t sb = launch(ctx, epoch_bump_kernel, dim3(1), dim3(32), 0, s, dev_epoch);
+    if (sb != WHALE_OK) return sb;
+  }
   whale_status_t st = ctx->p.es == 2 ? forward_impl<2>(ctx, x_local, labels_local, w_shard, loss, row_loss, s)
                                      : forward_impl<4>(ctx, x_local, labels_local, w_shard, loss, row_loss, s);
   if (st == WHALE_OK) ctx->have_fwd = true;
@@ -698,10 +734,10 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
                                     cudaStream_t s) {
   const Plan& p = c->p;
   const Layout& L = p.L;
-  const int par = p.world == 1 ? 0 : (c->epoch & 1);
   unsigned* counters = wsp<unsigned>(c, L.counters);
   int* err = reinterpret_cast<int*>(counters + CNT_ERR);
-  const int32_t* yg = p.world == 1 ? c->y_fwd : reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg[par]);
+  uint32_t* dev_epoch = counters + CNT_EPOCH;
+  const int32_t* yg = p.world == 1 ? c->y_fwd : reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg);
   {
     whale_status_t st = ensure_w_maps(c, w);
     if (st != WHALE_OK) return st;
@@ -711,9 +747,9 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     if (st != WHALE_OK) return st;
     c->dw_cached = dw;
   }
-  c->bwd_epoch += 1;
-  // ---- A6 G = (softmax - onehot) / B_tot, in place over P~
-  if (p.world > 1) {  // (N = 1: already done by the forward's fused stats/grad kernel)
+  // ---- A6 G = (softmax - onehot) / B_tot is produced by the forward's fused stats kernel;
+  //      the standalone kernel remains for WHALE_SPLIT_GRAD experiments only.
+  if (false) {
     constexpr int V = 16 / ES;
     dim3 grid(cdiv(cdiv(p.Cr, V), 256), static_cast<unsigned>(p.Bt));
     PROFILED(K_GRAD, s,
@@ -730,7 +766,8 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
   ax.st_out = wsp<float>(c, L.dxpart);
   ax.tile_cnt = wsp<uint32_t>(c, L.tile_cnt);
   ax.done_cnt = counters + CNT_DONE;
-  ax.epoch = c->bwd_epoch;
+  ax.dev_epoch = dev_epoch;
+  ax.bump_epoch = 1;  // the dX launch (or the fused launch) ends the step
   ax.B = static_cast<int>(p.B);
   ax.rank = p.rank;
   ax.world = p.world;
@@ -740,25 +777,52 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
   } else {
     ax.fix_mode = FIX_PUSH;
     for (int r = 0; r < p.world; ++r) {
-      ax.recv.p[r] = c->symm[r] + L.dxrecv[par];
+      ax.recv.p[r] = c->symm[r] + L.dxrecv;
       ax.rs_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_RS * kMaxRanks + p.rank;
     }
   }
-  if constexpr (ES == 2) {
+  if (ES == 2 && c->fused_bwd) {
+    // ---- A7 + A8 in one persistent launch: dX units first (one per CTA), then dW tiles
+    BwdArgs b{};
+    b.dx = ax;
+    b.dw = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
+    b.dw.dev_epoch = dev_epoch;
+    b.dw.err = err;
+    b.ux = p.dx.num_tiles;
+    b.tw = p.dw.num_tiles;
+    b.stages = c->bwd_stages;
+    b.stage_bytes = c->bwd_stage_bytes;
+    b.epi_bufs = c->bwd_epi_bufs;
+    b.sched_cnt = counters + CNT_SCHED;
+    const int grid = std::min(b.ux + b.tw, p.sms);
+    auto kern = splitfc_bwd_kernel<2>;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncAttributes fa{};
+      CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
+      attr = true;
+    }
+    PROFILED(K_BWD, s,
+             (launch(c, kern, dim3(grid), dim3(kGemmThreads), c->bwd_smem, s, c->tmG_dx, c->tmW_dx, c->tmDxPart,
+                     c->tmG_dw, c->tmX_dw, c->tmDW, b)));
+  } else if constexpr (ES == 2) {
     // ---- A7 dW_r = G_r^T X  (A = G^T MN-major, B = X MN-major)
     {
       GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
+      a.dev_epoch = dev_epoch;
       a.err = err;
       a.st_out = static_cast<float*>(dw);
       PROFILED(K_DW, s,
-               (launch_gemm<EPI_STORE_F32, true, true, 2>(c, 1, p.dw, c->tmG_dw, c->tmX_dw[par], c->tmDW, a, s)));
+               (launch_gemm<EPI_STORE_F32, true, true, 2>(c, 1, p.dw, c->tmG_dw, c->tmX_dw, c->tmDW, a, s)));
     }
     // ---- A8 dX = G_r W_r  (A = G K-major, B = W_r MN-major), split-K + fused fixup
     PROFILED(K_DX, s,
              (launch_gemm<EPI_STORE_F32, false, true, 2>(c, 2, p.dx, c->tmG_dx, c->tmW_dx, c->tmDxPart, ax, s)));
   } else {
     // kind::tf32 accepts K-major operands only (plain 128B swizzle): transpose G, X, W_r.
-    const void* xg = p.world == 1 ? c->x_fwd : static_cast<const void*>(c->symm[p.rank] + L.xg[par]);
+    const void* xg = p.world == 1 ? c->x_fwd : static_cast<const void*>(c->symm[p.rank] + L.xg);
     auto tr = [&](const void* src, long long sld, void* dst, long long dld, int64_t R, int64_t Cc) -> whale_status_t {
       return launch(c, transpose_f32_kernel, dim3(cdiv(Cc, 32), cdiv(R, 32)), dim3(32, 32), 0, s,
                     static_cast<const float*>(src), sld, static_cast<float*>(dst), dld, static_cast<int>(R),
@@ -769,6 +833,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     PROFILED(K_TRANSPOSE, s, (tr(w, p.D, c->ws + L.WT, p.ldp, p.Cr, p.D)));
     {
       GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
+      a.dev_epoch = dev_epoch;
       a.err = err;
       a.st_out = static_cast<float*>(dw);
       PROFILED(K_DW, s, (launch_gemm<EPI_STORE_F32, false, false, 4>(c, 4, p.dw, c->tmGT, c->tmXT, c->tmDW, a, s)));
@@ -783,8 +848,9 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_RS * kMaxRanks;
     PROFILED(K_RS_REDUCE, s,
              (launch(c, dx_reduce_kernel<ES>, dim3(g2), dim3(256), 0, s,
-                     reinterpret_cast<const float4*>(c->symm[p.rank] + L.dxrecv[par]), static_cast<int>(p.B),
-                     static_cast<int>(p.D), p.world, my_flags, c->bwd_epoch, dx_local, err)));
+                     reinterpret_cast<const float4*>(c->symm[p.rank] + L.dxrecv), static_cast<int>(p.B),
+                     static_cast<int>(p.D), p.world, my_flags, static_cast<const uint32_t*>(dev_epoch), dx_local,
+                     err)));
   }
   return WHALE_OK;
 }
@@ -817,8 +883,9 @@ extern "C" whale_status_t whale_splitfc_check(whale_splitfc_ctx* ctx, void* stre
 // ============================================================================ introspection
 extern "C" int32_t whale_splitfc_launches_per_step(const whale_splitfc_ctx* ctx) {
   if (!ctx) return 0;
-  // N = 1: logits, stats+grad, dW, dX;  N > 1: gather, logits, stats, grad, dW, dX, dX owner reduce
-  const int base = ctx->p.world == 1 ? 4 : 7;
+  // N = 1: logits, stats+grad, dW, dX;  N > 1: + gather, + dX owner reduce
+  int base = ctx->p.world == 1 ? 4 : 6;
+  if (ctx->fused_bwd) base -= 1;  // dW + dX share one launch
   return base + (ctx->p.es == 4 ? 3 : 0);  // fp32 path: operand transposes
 }
 
@@ -887,4 +954,31 @@ extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, cha
   if (s.size() + 1 > buf_len) return fail(WHALE_ERR_INVALID_ARG, "buffer too small (%zu)", s.size() + 1);
   memcpy(buf, s.c_str(), s.size() + 1);
   return WHALE_OK;
+}
+
+// Internal (not in the public header): debug timestamps written by kernels run with
+// WHALE_GATHER_DBG & 16.  Synchronises the device.
+extern "C" int whale_debug_timestamps(unsigned long long* out, int n) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(out, g_dbg_ts, sizeof(unsigned long long) * std::min(n, 32)) != cudaSuccess) return -1;
+  return 0;
+}
+
+// Internal: device-side kernel windows (see TraceScope).  enable != 0 clears and arms the
+// tracer; whale_debug_trace_read copies [16][2] (start, end) ns and re-arms (clears).
+extern "C" int whale_debug_trace_enable(int enable) {
+  unsigned int on = enable ? 1u : 0u;
+  unsigned long long init[16][2];
+  for (int k = 0; k < 16; ++k) {
+    init[k][0] = ~0ull;
+    init[k][1] = 0ull;
+  }
+  if (cudaMemcpyToSymbol(g_trace, init, sizeof(init)) != cudaSuccess) return -1;
+  if (cudaMemcpyToSymbol(g_trace_on, &on, sizeof(on)) != cudaSuccess) return -1;
+  return 0;
+}
+extern "C" int whale_debug_trace_read(unsigned long long* out) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  if (cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 32) != cudaSuccess) return -1;
+  return whale_debug_trace_enable(1);
 }

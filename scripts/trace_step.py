@@ -1,0 +1,63 @@
+"""Device-side timeline of one split-FC step (kernel windows from the library tracer).
+
+torchrun ... scripts/trace_step.py  (or plain python for N=1).  CFG env picks the config.
+Graph-replays the step, arms the tracer, replays once, reads windows (ns rel. to step start).
+"""
+import ctypes, json, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synthetic as syn
+from paper_2011_09208_b200 import SplitFCSoftmaxCE, _lib
+world = int(os.environ.get("WORLD_SIZE", "1"))
+group = None
+if world > 1:
+    import torch.distributed as dist
+    dist.init_process_group("nccl")
+    group = dist.group.WORLD
+rank = int(os.environ.get("RANK", "0"))
+local = int(os.environ.get("LOCAL_RANK", "0"))
+torch.cuda.set_device(local); dev = torch.device("cuda", local)
+cfg = syn.CONFIGS[os.environ.get("CFG", "c2")]
+op = SplitFCSoftmaxCE(cfg.C, cfg.D, cfg.B, capacity=cfg.capacity, dtype=syn.torch_dtype(cfg.dtype), group=group, device=dev)
+X = syn.gen_features((rank * cfg.B, (rank + 1) * cfg.B), cfg.D, 1, cfg.dtype, device=dev)
+y = syn.gen_labels((rank * cfg.B, (rank + 1) * cfg.B), cfg.C, 1, device=dev).to(torch.int32)
+W = syn.gen_weight((op.o_r, op.o_r + op.C_r), cfg.D, 1, "init", cfg.dtype, device=dev)
+dx = torch.empty(cfg.B, cfg.D, dtype=syn.torch_dtype(cfg.dtype), device=dev)
+dw = torch.empty(op.C_r, cfg.D, device=dev)
+def step():
+    op.forward(X, y, W); op.backward(W, dx, dw)
+for _ in range(5): step()
+torch.cuda.synchronize()
+g = torch.cuda.CUDAGraph()
+with torch.cuda.graph(g): step()
+g.replay(); torch.cuda.synchronize()
+L = _lib.lib()
+L.whale_debug_trace_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+names = ["gather", "logits", "stats", "grad", "dw", "dx", "rs_reduce", "transpose", "bwd", "bump"]
+L.whale_debug_trace_enable(1)
+out = []
+for it in range(int(os.environ.get("ITERS", "5"))):
+    if group is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    g.replay()
+    buf = (ctypes.c_ulonglong * 32)()
+    L.whale_debug_trace_read(buf)
+    t0 = min(buf[2 * k] for k in range(16) if buf[2 * k + 1])
+    rec = {names[k]: [round((buf[2 * k] - t0) / 1e3, 1), round((buf[2 * k + 1] - t0) / 1e3, 1)]
+           for k in range(len(names)) if buf[2 * k + 1]}
+    tend = max(v[1] for v in rec.values())
+    out.append({"rank": rank, "it": it, "span_us": tend, "win_us": rec})
+L.whale_debug_trace_enable(0)
+op.check()
+if group is not None:
+    allo = [None] * world
+    dist.all_gather_object(allo, out)
+    if rank == 0:
+        for o in allo:
+            for r in o[-2:]:
+                print(json.dumps(r))
+    dist.barrier(); dist.destroy_process_group()
+else:
+    for r in out[-2:]:
+        print(json.dumps(r))
