@@ -59,7 +59,7 @@ class ClockSampler:
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, dev_index: int, period_s: float = 0.005):
+    def __init__(self, dev_index: int, period_s: float = 0.001):
         self.samples, self.reasons, self.ok = [], set(), False
         self.period = period_s
         self.dev = dev_index

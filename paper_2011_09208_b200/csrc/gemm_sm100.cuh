@@ -249,7 +249,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
       const int box_bytes = bk * kRowBytes;
       const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
-      const uint32_t tx = static_cast<uint32_t>(a_bytes + (B_MN ? (a.BN / kAtom) * box_bytes : a.BN * kRowBytes));
+      const uint32_t tx = static_cast<uint32_t>(((a.debug & 8) ? 0 : a_bytes) +
+                                                (B_MN ? (a.BN / kAtom) * box_bytes : a.BN * kRowBytes));
       for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
         int mb, nb, sp, kb0, kb1;
         decode_tile(a, tile, mb, nb, sp, kb0, kb1);
@@ -258,7 +259,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* sA = smem + stage * a.stage_bytes;
           uint8_t* sB = sA + a_bytes;
           mbar_arrive_expect_tx(&full[stage], tx);
-          if (!A_MN) {
+          if (a.debug & 8) {
+            // timing experiment: A operand not loaded
+          } else if (!A_MN) {
             tma_load_2d(sA, &tmA, &full[stage], kb * kBK, mb * kBM);
           } else {
 #pragma unroll
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t aS = smem_u32(smem + stage * a.stage_bytes);
           const uint32_t bS = aS + a_bytes;
 #pragma unroll 4
-          for (int k = 0; k < kmma; ++k) {  // MMAs of 32 bytes of K
+          for (int k = 0; k < ((a.debug & 4) ? 0 : kmma); ++k) {  // MMAs of 32 bytes of K
             const uint64_t ad = A_MN ? umma_sdesc(aS + k * kKStepMN, box_bytes, 1024)
                                      : umma_sdesc(aS + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_sdesc(bS + k * kKStepMN, box_bytes, 1024)

@@ -48,6 +48,17 @@ __device__ __forceinline__ bool last_block_ticket(unsigned* counter) {
   return is_last;
 }
 
+// Same, over a subset of n participating CTAs (e.g. the chunk-0 CTA of every row).
+__device__ __forceinline__ bool last_of_n(unsigned* counter, unsigned n) {
+  __shared__ bool is_last_n;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last_n = (atomicAdd(counter, 1u) == n - 1);
+  __syncthreads();
+  if (is_last_n) __threadfence();
+  return is_last_n;
+}
+
 // ---------------------------------------------------------------- A2 bridge gather
 // Rank r writes its B rows at row offset r*B of every rank's gathered X buffer, and its
 // labels likewise; the last block then raises flag[GATHER][r] = epoch on every peer.
@@ -331,7 +342,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
     }
   }
   // ---- mean loss: last CTA, fixed order
-  if (!last_block_ticket<false>(a.counter)) return;
+  if (blockIdx.x != 0 || !last_of_n(a.counter, gridDim.y)) return;  // loss: chunk-0 CTAs only
   double acc = 0.0;
   for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) acc += static_cast<double>(__ldcg(a.row_loss_all + r));
   __shared__ double part[4];
@@ -366,6 +377,8 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
   const int i = blockIdx.x;
   const int chunk_id = blockIdx.y;
   const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;
+  const int tslot = (g_trace_on && chunk_id == 0 && threadIdx.x == 0) ? (i == 0 ? 16 : (i == a.Bt - 1 ? 24 : -1)) : -1;
+  if (tslot >= 0) g_dbg_ts[tslot] = gtime_ns();
   const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
   const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
   const long long y = a.y[i];
@@ -388,22 +401,33 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
     for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads)
       s += __ldg(st + t) * __expf(__ldg(mt + t) - m);
     s = block_sum128(s, red);
-    if (threadIdx.x < a.world) {  // thread p pushes the record + flag to peer p
+    if (tslot >= 0) g_dbg_ts[tslot + 1] = gtime_ns();
+    if (threadIdx.x < a.world) {  // thread p pushes the record to peer p
       if (threadIdx.x == 0 && (y < 0 || y >= a.C)) atomicOr(a.err, ERR_LABEL);
       const bool own = (y >= a.o_r) && (y < a.o_r + a.C_r);
       const float zy = own ? a.zy_r[i] : 0.f;
       const int p = threadIdx.x;
-      reinterpret_cast<float4*>(a.peer_stats.p[p])[static_cast<size_t>(a.rank) * a.Bt + i] = make_float4(m, s, zy, 0.f);
-      __threadfence_system();  // record before flag (fence + relaxed: cheaper than a release store)
-      st_relaxed_sys(row_flags.p[p] + i, e);
+      // LL-style: three 8-byte {value, epoch} words; each 8-byte store is single-copy atomic,
+      // so the reader validates every word by its epoch half -- no fence, no separate flag
+      uint2* dst = reinterpret_cast<uint2*>(a.peer_stats.p[p]) + (static_cast<size_t>(a.rank) * a.Bt + i) * 4;
+      st_relaxed_sys_v2(dst + 0, __float_as_uint(m), e);
+      st_relaxed_sys_v2(dst + 1, __float_as_uint(s), e);
+      st_relaxed_sys_v2(dst + 2, __float_as_uint(zy), e);
     }
+    if (tslot >= 0) g_dbg_ts[tslot + 2] = gtime_ns();
   }
   // ---- acquire the row's records from every rank, combine in rank order
+  (void)row_flags;
+  (void)my_row_flags;
   if (threadIdx.x < a.world) {
-    wait_flag_geq(my_row_flags + static_cast<size_t>(threadIdx.x) * a.Bt + i, e, a.err, ERR_COMM);
-    recs[threadIdx.x] = __ldcg(a.my_stats + static_cast<size_t>(threadIdx.x) * a.Bt + i);
+    const uint2* src = reinterpret_cast<const uint2*>(a.my_stats) + (static_cast<size_t>(threadIdx.x) * a.Bt + i) * 4;
+    const float mv = __uint_as_float(wait_ll(src + 0, e, a.err, ERR_COMM));
+    const float sv = __uint_as_float(wait_ll(src + 1, e, a.err, ERR_COMM));
+    const float zv = __uint_as_float(wait_ll(src + 2, e, a.err, ERR_COMM));
+    recs[threadIdx.x] = make_float4(mv, sv, zv, 0.f);
   }
   __syncthreads();
+  if (tslot >= 0) g_dbg_ts[tslot + 3] = gtime_ns();
   float mm = -INFINITY;
   for (int p = 0; p < a.world; ++p) mm = fmaxf(mm, recs[p].x);
   float ss = 0.f, zz = 0.f;
@@ -447,7 +471,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
       *p = f;
     }
   }
-  if (!last_block_ticket<false>(a.counter)) return;
+  if (chunk_id != 0 || !last_of_n(a.counter, gridDim.x)) return;  // loss: chunk-0 CTAs only
   double acc = 0.0;
   for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) acc += static_cast<double>(__ldcg(a.row_loss_all + r));
   __shared__ double part[4];

@@ -215,6 +215,30 @@ __device__ __forceinline__ void red_add_relaxed_sys(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// LL protocol word: {data (low 32), flag (high 32)} written by one aligned 64-bit store, which
+// is single-copy atomic -- the reader validates the data by its flag half (NCCL's LL idea).
+__device__ __forceinline__ void st_relaxed_sys_v2(uint2* p, uint32_t data, uint32_t flag) {
+  const unsigned long long w = (static_cast<unsigned long long>(flag) << 32) | data;
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const void* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until the LL word carries `flag`; returns its data half.
+__device__ __forceinline__ uint32_t wait_ll(const uint2* p, uint32_t flag, int* err_word, int code) {
+  unsigned long long w = ld_relaxed_sys_u64(p);
+  if (static_cast<uint32_t>(w >> 32) != flag) {
+    SpinGuard g;
+    do {
+      __nanosleep(20);
+      g.check(err_word, code);
+      w = ld_relaxed_sys_u64(p);
+    } while (static_cast<uint32_t>(w >> 32) != flag);
+  }
+  return static_cast<uint32_t>(w);
+}
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -224,7 +248,10 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void wait_flag_geq(const uint32_t* p, uint32_t epoch, int* err_word, int code) {
   if (static_cast<int32_t>(ld_acquire_sys(p) - epoch) >= 0) return;
   SpinGuard g;
-  while (static_cast<int32_t>(ld_acquire_sys(p) - epoch) < 0) g.check(err_word, code);
+  while (static_cast<int32_t>(ld_acquire_sys(p) - epoch) < 0) {
+    __nanosleep(40);  // many CTAs may poll: keep L2 / NVLink free for the incoming data
+    g.check(err_word, code);
+  }
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {

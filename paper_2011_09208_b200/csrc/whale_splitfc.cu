@@ -274,7 +274,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
     L.rowflags = take(static_cast<size_t>(p.world) * p.Bt * 4);
     L.xg = take(static_cast<size_t>(p.Bt) * p.D * p.es);
     L.yg = take(p.Bt * 4);
-    L.stats = take(static_cast<size_t>(p.world) * p.Bt * 16);
+    L.stats = take(static_cast<size_t>(p.world) * p.Bt * 32);  // LL words {m,s,zy,-} x {data, epoch}
     L.dxrecv = take(static_cast<size_t>(p.world) * p.B * p.D * 4);
   }
   L.symm_total = o;

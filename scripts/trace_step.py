@@ -33,6 +33,7 @@ with torch.cuda.graph(g): step()
 g.replay(); torch.cuda.synchronize()
 L = _lib.lib()
 L.whale_debug_trace_read.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+L.whale_debug_timestamps.argtypes = [ctypes.POINTER(ctypes.c_ulonglong), ctypes.c_int]
 names = ["gather", "logits", "stats", "grad", "dw", "dx", "rs_reduce", "transpose", "bwd", "bump"]
 L.whale_debug_trace_enable(1)
 out = []
@@ -43,11 +44,15 @@ for it in range(int(os.environ.get("ITERS", "5"))):
     g.replay()
     buf = (ctypes.c_ulonglong * 32)()
     L.whale_debug_trace_read(buf)
+    st = (ctypes.c_ulonglong * 32)()
+    L.whale_debug_timestamps(st, 32)
     t0 = min(buf[2 * k] for k in range(16) if buf[2 * k + 1])
     rec = {names[k]: [round((buf[2 * k] - t0) / 1e3, 1), round((buf[2 * k + 1] - t0) / 1e3, 1)]
            for k in range(len(names)) if buf[2 * k + 1]}
     tend = max(v[1] for v in rec.values())
-    out.append({"rank": rank, "it": it, "span_us": tend, "win_us": rec})
+    stamps = {"row0": [round((st[16 + j] - t0) / 1e3, 1) for j in range(4) if st[16 + j] >= t0],
+              "rowLast": [round((st[24 + j] - t0) / 1e3, 1) for j in range(4) if st[24 + j] >= t0]}
+    out.append({"rank": rank, "it": it, "span_us": tend, "win_us": rec, "stats_stamps": stamps})
 L.whale_debug_trace_enable(0)
 op.check()
 if group is not None:

@@ -1,0 +1,32 @@
+"""Multi-GPU parity (N = 2 / 4 / 8 on one box): launches scripts/mgpu_parity.py under
+torchrun with one rank per visible GPU; each rank checks its dX_r rows and dW_r shard
+against the unsharded fp64 oracle and the loss must be bit-identical on all ranks
+(even, uneven 2:1:..., fp32 and the c2 shape).  Skipped with fewer than 2 GPUs."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
+def test_multigpu_parity():
+    n = min(torch.cuda.device_count(), 8)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(n), "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "scripts", "mgpu_parity.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert '"ok": false' not in r.stdout
