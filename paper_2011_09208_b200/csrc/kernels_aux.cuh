@@ -121,6 +121,7 @@ struct StatsArgs {
   float* row_loss_local; // [B] or NULL
   unsigned* counter;
   int* err;
+  int grad_vecs;         // 16-byte vectors of P~ per thread in the fused gradient (chunk size)
 };
 
 constexpr int kStatsThreads = 128;
@@ -312,9 +313,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
     if (a.row_loss_local) a.row_loss_local[i] = l - zy;
   }
   // ---- G for this CTA's chunk of the row
-  const long long chunk = static_cast<long long>(kStatsThreads) * kGradVecs * V;
-#pragma unroll
-  for (int k = 0; k < kGradVecs; ++k) {
+  const long long chunk = static_cast<long long>(kStatsThreads) * a.grad_vecs * V;
+#pragma unroll 4
+  for (int k = 0; k < a.grad_vecs; ++k) {
     const long long j0 = blockIdx.x * chunk + (static_cast<long long>(k) * kStatsThreads + threadIdx.x) * V;
     if (j0 >= a.C_r) break;
     const float scale = __expf(__ldg(mt + j0 / BN) - l) * inv_bt;
@@ -442,9 +443,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
     if (a.row_loss_local && i >= a.rank * a.B && i < (a.rank + 1) * a.B) a.row_loss_local[i - a.rank * a.B] = l - zz;
   }
   // ---- G for this CTA's chunk of the row
-  const long long chunk = static_cast<long long>(kStatsThreads) * kGradVecs * V;
-#pragma unroll
-  for (int k = 0; k < kGradVecs; ++k) {
+  const long long chunk = static_cast<long long>(kStatsThreads) * a.grad_vecs * V;
+#pragma unroll 4
+  for (int k = 0; k < a.grad_vecs; ++k) {
     const long long j0 = chunk_id * chunk + (static_cast<long long>(k) * kStatsThreads + threadIdx.x) * V;
     if (j0 >= a.C_r) break;
     const float scale = __expf(__ldg(mt + j0 / BN) - l) * inv_bt;

@@ -458,6 +458,7 @@ static int env_int(const char* name, int dflt) {
 }
 static int g_n_fastest = env_int("WHALE_N_FASTEST", 0);
 static int g_epi_debug = env_int("WHALE_EPI_DEBUG", 0);
+static int g_dw_m_fastest = env_int("WHALE_DW_M_FASTEST", 0);
 
 static GemmArgs base_args(const GemmCfg& g, int M, int N) {
   GemmArgs a{};
@@ -685,9 +686,12 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.row_loss_local = row_loss;
     a.counter = counters + CNT_STATS;
     a.err = err;
+    // every CTA re-reads its row's T tile partials (8T bytes): size the chunk so that this
+    // stays <= ~10% of the chunk's P~ read+write traffic (4096 B per vector of the 128 threads)
+    a.grad_vecs = static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(4, (p.fwd.n_blocks * 10 + 511) / 512)));
+    const int64_t chunk = static_cast<int64_t>(kStatsThreads) * a.grad_vecs * (16 / ES);
     if (p.world == 1) {
       // A4-A6 fused: lse, loss and G in one pass (no exchange needed)
-      const int64_t chunk = static_cast<int64_t>(kStatsThreads) * kGradVecs * (16 / ES);
       PROFILED(K_STATS, s,
                (launch(c, stats_grad_kernel<ES>, dim3(cdiv(p.Cr, chunk), p.Bt), dim3(kStatsThreads), 0, s, a,
                        static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
@@ -697,7 +701,6 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
       PeerFlags rf{};
       for (int r = 0; r < p.world; ++r)
         rf.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.rowflags) + static_cast<size_t>(p.rank) * p.Bt;
-      const int64_t chunk = static_cast<int64_t>(kStatsThreads) * kGradVecs * (16 / ES);
       PROFILED(K_STATS, s,
                (launch(c, stats_grad_multi_kernel<ES>, dim3(p.Bt, cdiv(p.Cr, chunk)), dim3(kStatsThreads), 0, s, a,
                        static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
@@ -787,6 +790,9 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     b.dx = ax;
     b.dw = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
     b.dw.dev_epoch = dev_epoch;
+    // dW tiles N-fastest: CTAs running together share one G^T class block (read from HBM
+    // once) across all D-column blocks; M-fastest re-read G once per column block (c5: 16x)
+    b.dw.n_fastest = g_dw_m_fastest ? 0 : 1;
     b.dw.err = err;
     b.ux = p.dx.num_tiles;
     b.tw = p.dw.num_tiles;
