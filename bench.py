@@ -417,7 +417,7 @@ def run_reference(args, cfg, seed, world, rank):
     """Reference arm: the fp64 CPU oracle as it stands, on the host cores, bounded sample per step."""
     if rank != 0:
         return
-    rows = 8
+    rows = min(cfg.B * world, 32)  # same sample as the cpu_baseline leg
     import oracle
     X = syn.gen_features((0, rows), cfg.D, seed, cfg.dtype).double().numpy()
     y = syn.gen_labels((0, rows), cfg.C, seed).numpy()
