@@ -84,6 +84,9 @@ struct GemmArgs {
   PeerFlags rs_flags;       // FIX_PUSH: &flag[RS][rank] on every rank
   int store_mode;           // EPI_STORE_F32: 0 per-warp TMA box, 1 CTA-wide TMA box, 2 st.global
   int n_fastest;            // tile order: 0 = M fastest (share B), 1 = N fastest (share A)
+  int cluster;              // 1, or 2: CTA pairs take M-adjacent tiles and TMA-multicast B
+                            // (each CTA loads half of the B tile into both CTAs' smem);
+                            // num_tiles then counts pair tiles (m_blocks must be even)
   int debug;                // timing experiments only: bit0 skip stores, bit1 skip TMEM loads
   float* st_out;            // store_mode 2: output base ([splits x] M x N fp32)
   int* err;
@@ -119,6 +122,31 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, int tile, int& mb
   }
   kb0 = sp * a.kb_per_split;
   kb1 = min(kb0 + a.kb_per_split, a.num_kb);
+}
+
+// Unit -> tile for a CTA of rank `crank` in its cluster: with pairs (cluster = 2) a unit is
+// an M-adjacent tile pair (2 mp, nb), (2 mp + 1, nb) sharing the B tile.
+__device__ __forceinline__ void decode_unit(const GemmArgs& a, int unit, uint32_t crank, int& mb, int& nb, int& sp,
+                                            int& kb0, int& kb1) {
+  if (a.cluster == 2) {
+    const int mpairs = a.m_blocks / 2;
+    if (a.n_fastest) {
+      nb = unit % a.n_blocks;
+      const int r = unit / a.n_blocks;
+      mb = r % mpairs;
+      sp = r / mpairs;
+    } else {
+      mb = unit % mpairs;
+      const int r = unit / mpairs;
+      nb = r % a.n_blocks;
+      sp = r / a.n_blocks;
+    }
+    mb = 2 * mb + static_cast<int>(crank);
+    kb0 = sp * a.kb_per_split;
+    kb1 = min(kb0 + a.kb_per_split, a.num_kb);
+  } else {
+    decode_tile(a, unit, mb, nb, sp, kb0, kb1);
+  }
 }
 
 // Wait until <= n bulk stores of this thread are still reading smem (n = bufs - 1).
@@ -208,11 +236,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int kKStepMN = (32 / ES) * kRowBytes;  // MN-major: UMMA_K rows per MMA
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  // CTA pairs (cluster = 2): unit u = pair tile, this CTA takes M block 2*mp + crank
+  const int cs = a.cluster;
+  const uint32_t crank = cs > 1 ? cluster_ctarank() : 0u;
+  const int unit0 = cs > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int ustride = cs > 1 ? static_cast<int>(ncluster_x()) : static_cast<int>(gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], cs);  // pairs: both CTAs' MMAs must release a stage (multicast B)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -228,6 +261,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 2) tmem_alloc(tmem_holder, kTmemCols);
   tc_fence_before();
   __syncthreads();
+  if (cs > 1) cluster_sync();  // peer barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   pdl_wait();      // everything below reads/writes memory the previous kernel may touch
@@ -251,9 +285,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
       const uint32_t tx = static_cast<uint32_t>(((a.debug & 8) ? 0 : a_bytes) +
                                                 (B_MN ? (a.BN / kAtom) * box_bytes : a.BN * kRowBytes));
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x) {
+      for (int tile = unit0; tile < a.num_tiles; tile += ustride) {
         int mb, nb, sp, kb0, kb1;
-        decode_tile(a, tile, mb, nb, sp, kb0, kb1);
+        decode_unit(a, tile, crank, mb, nb, sp, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* sA = smem + stage * a.stage_bytes;
@@ -268,7 +302,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int j = 0; j < kBM / kAtom; ++j)
               tma_load_2d(sA + j * box_bytes, &tmA, &full[stage], mb * kBM + j * kAtom, kb * bk);
           }
-          if (!B_MN) {
+          if (cs > 1) {
+            // B is shared by the pair: this CTA loads its half and multicasts it to both
+            if (!B_MN) {  // tmB box = {kBK, BN/2}
+              const int half = a.BN / 2;
+              tma_load_2d_mc(sB + crank * half * kRowBytes, &tmB, &full[stage], kb * kBK,
+                             nb * a.BN + static_cast<int>(crank) * half, 0x3);
+            } else {
+              for (int j = static_cast<int>(crank); j < a.BN / kAtom; j += 2)
+                tma_load_2d_mc(sB + j * box_bytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * bk, 0x3);
+            }
+          } else if (!B_MN) {
             tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
           } else {
             for (int j = 0; j < a.BN / kAtom; ++j)
@@ -292,9 +336,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = unit0; tile < a.num_tiles; tile += ustride, ++it) {
         int mb, nb, sp, kb0, kb1;
-        decode_tile(a, tile, mb, nb, sp, kb0, kb1);
+        decode_unit(a, tile, crank, mb, nb, sp, kb0, kb1);
         const int acc = it & 1;
         const uint32_t aph = (it >> 1) & 1;
         mbar_wait(&tempty[acc], aph ^ 1u);
@@ -316,7 +360,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             else
               umma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);  // frees this smem stage once the MMAs have read it
+          // frees this smem stage once the MMAs have read it (pairs: in both CTAs, since the
+          // peer multicasts its half of B into this stage too)
+          if (cs > 1) umma_commit_mc(&empty[stage], 0x3);
+          else umma_commit(&empty[stage]);
           if (++stage == a.stages) {
             stage = 0;
             phase ^= 1u;
@@ -332,9 +379,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint8_t* ebuf = epi_smem + q * nbuf * kEpiBufBytes;
     int buf = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < a.num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = unit0; tile < a.num_tiles; tile += ustride, ++it) {
       int mb, nb, sp, kb0, kb1;
-      decode_tile(a, tile, mb, nb, sp, kb0, kb1);
+      decode_unit(a, tile, crank, mb, nb, sp, kb0, kb1);
       const int acc = it & 1;
       const uint32_t aph = (it >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
@@ -523,6 +570,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  // pairs: the peer may still multicast into this CTA's smem / arrive on its barriers
+  if (cs > 1) cluster_sync();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);

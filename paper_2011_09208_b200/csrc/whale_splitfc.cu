@@ -86,7 +86,26 @@ extern "C" whale_status_t whale_splitfc_plan(int64_t num_classes, int32_t world_
 struct GemmCfg {
   int BN = 0, bk = 64, m_blocks = 0, n_blocks = 0, splits = 1, num_kb = 0, kb_per_split = 0, num_tiles = 0;
   int stages = 0, stage_bytes = 0, epi_bufs = 2, smem = 0, grid = 0;
+  int cluster = 1;  // 2: CTA pairs share (TMA-multicast) the B tile of M-adjacent tiles
 };
+
+static int env_int(const char* name, int dflt);
+
+// Pair M-adjacent tiles in 2-CTA clusters when the tile grid allows it (even m_blocks, B
+// tile splittable in halves / atom pairs); grid = 2 x pair tiles, capped at the SM count.
+static void maybe_pair(GemmCfg& g, int sms, bool b_mn, int atom) {
+  // off by default: measured neutral for the logits (c5: tensor-bound at the sustained
+  // peak) and +3% for the standalone dW GEMM; kept as an option (WHALE_CLUSTER=1)
+  const bool ok = env_int("WHALE_CLUSTER", 0) != 0 && g.m_blocks >= 2 &&
+                  (b_mn ? (g.BN / atom) % 2 == 0 : (g.BN / 2) % 16 == 0) && g.splits == 1;
+  if (!ok) return;
+  g.cluster = 2;
+  // an odd M block count gets one all-padding tile (TMA zero-fills its loads, clips its stores)
+  g.m_blocks += g.m_blocks & 1;
+  g.num_tiles = g.m_blocks * g.n_blocks * g.splits;
+  const int units = g.num_tiles / 2;
+  g.grid = 2 * std::min(units, sms / 2);
+}
 
 struct Layout {
   // local workspace offsets
@@ -234,6 +253,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   const int kbk = kRowBytes / p.es;   // K elements per stage
   const int atom = kRowBytes / p.es;  // MN-major atom / fwd P~ chunk
   p.fwd = choose_plain(p.Bt, p.Cr, p.D, atom, kbk, sms);
+  maybe_pair(p.fwd, sms, false, atom);
   {
     // dW: both operands MN-major; a short K (= B_tot <= 32) uses 32-row K stages (no
     // zero-padded half stage), which doubles the pipeline depth for the same smem.
@@ -427,7 +447,23 @@ static whale_status_t launch_gemm(whale_splitfc_ctx* c, int slot, const GemmCfg&
                                   kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
     g_attr_done[slot] = true;
   }
-  return launch(c, kern, dim3(g.grid), dim3(kGemmThreads), g.smem, s, A, B, O, args);
+  if (g.cluster <= 1) return launch(c, kern, dim3(g.grid), dim3(kGemmThreads), g.smem, s, A, B, O, args);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = g.cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->pdl ? 2 : 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A, B, O, args));
+  return WHALE_OK;
 }
 
 static void prof_begin(whale_splitfc_ctx* c, int kind, cudaStream_t s, ProfRec& r) {
@@ -470,7 +506,8 @@ static GemmArgs base_args(const GemmCfg& g, int M, int N) {
   a.splits = g.splits;
   a.num_kb = g.num_kb;
   a.kb_per_split = g.kb_per_split;
-  a.num_tiles = g.num_tiles;
+  a.num_tiles = g.cluster > 1 ? g.num_tiles / g.cluster : g.num_tiles;  // units (pair tiles)
+  a.cluster = g.cluster;
   a.stages = g.stages;
   a.stage_bytes = g.stage_bytes;
   a.epi_bufs = g.epi_bufs;
@@ -529,6 +566,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     c->bwd_smem = fixed + c->bwd_stages * c->bwd_stage_bytes;
     if (c->bwd_stages < 2) c->fused_bwd = false;
   }
+  if (!c->fused_bwd && p.es == 2) maybe_pair(c->p.dw, sms, true, kRowBytes / p.es);  // standalone dW GEMM
   // static TMA maps
   const int es = p.es, kbk = kRowBytes / es, atom = kRowBytes / es;
   if (p.world > 1) {
@@ -571,7 +609,9 @@ static whale_status_t ensure_w_maps(whale_splitfc_ctx* c, const void* w) {
   if (w == c->w_cached) return WHALE_OK;
   const Plan& p = c->p;
   const int kbk = kRowBytes / p.es, atom = kRowBytes / p.es;
-  whale_status_t st = map2d(&c->tmW_fwd, w, p.es, p.D, p.Cr, p.D * p.es, kbk, p.fwd.BN);
+  // paired forward: each CTA of the pair loads (and multicasts) half of the W tile
+  const uint32_t box_rows = p.fwd.cluster > 1 ? p.fwd.BN / 2 : p.fwd.BN;
+  whale_status_t st = map2d(&c->tmW_fwd, w, p.es, p.D, p.Cr, p.D * p.es, kbk, box_rows);
   if (st != WHALE_OK) return st;
   st = map2d(&c->tmW_dx, w, p.es, p.D, p.Cr, p.D * p.es, atom, kbk);
   if (st != WHALE_OK) return st;
@@ -940,9 +980,9 @@ extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, cha
     char b[320];
     snprintf(b, sizeof(b),
              "{\"BN\":%d,\"bk\":%d,\"m_blocks\":%d,\"n_blocks\":%d,\"splits\":%d,\"num_kb\":%d,\"kb_per_split\":%d,"
-             "\"tiles\":%d,\"stages\":%d,\"epi_bufs\":%d,\"smem\":%d,\"grid\":%d}",
+             "\"tiles\":%d,\"stages\":%d,\"epi_bufs\":%d,\"smem\":%d,\"grid\":%d,\"cluster\":%d}",
              c.BN, c.bk, c.m_blocks, c.n_blocks, c.splits, c.num_kb, c.kb_per_split, c.num_tiles, c.stages, c.epi_bufs,
-             c.smem, c.grid);
+             c.smem, c.grid, c.cluster);
     return std::string(b);
   };
   char head[320];
