@@ -73,6 +73,31 @@ whale_status_t whale_splitfc_plan(int64_t num_classes, int32_t world_size, const
                                   int64_t* shard_counts, int64_t* shard_offsets);
 
 /*
+ * whale_splitfc_plan_mem -- class-shard sizes under per-device memory caps (pure host
+ * function; deterministic; thread-safe).
+ *
+ * Algorithm 1, "Memory-Constraint Load Balancing", subject to the
+ * constraint of Formula 1, L_i * TG_mem <= DM_i: start from the
+ * proportional plan above; while some device is over its memory and some device has room,
+ * shift classes from the device with the highest memory utilisation (peak) to the free
+ * device with the lowest (FLOP utilisation, memory utilisation) (valley); each shift moves
+ * min(peak overload, valley headroom) whole classes.
+ *
+ *   mem_bytes        [N] memory available to the FC shard on each device, or NULL (no cap:
+ *                    identical to whale_splitfc_plan)
+ *   bytes_per_class  device bytes one class costs (e.g. 6*D for a bf16 W row + fp32 dW row)
+ *   fixed_bytes      bytes every device needs regardless of its shard (workspaces)
+ *   capacity, outputs as whale_splitfc_plan.
+ * Ties go to the lower rank; exact integer/rational arithmetic (R13).
+ * Errors: as whale_splitfc_plan; WHALE_ERR_INVALID_ARG if bytes_per_class == 0;
+ *         WHALE_ERR_UNSPLITTABLE if a device stays over its cap (infeasible) or ends with 0
+ *         classes.
+ */
+whale_status_t whale_splitfc_plan_mem(int64_t num_classes, int32_t world_size, const uint32_t* capacity,
+                                      const uint64_t* mem_bytes, uint64_t bytes_per_class, uint64_t fixed_bytes,
+                                      int64_t* shard_counts, int64_t* shard_offsets);
+
+/*
  * Context descriptor.  Layouts (all row-major, leading dimension = row length):
  *   X_r   [B x D]    x_dtype      this rank's DP rows (the backbone's output)
  *   y_r   [B]        int32        global class ids in [0, C)

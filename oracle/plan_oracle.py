@@ -54,3 +54,65 @@ def plan_shards(num_classes: int, world_size: int, capacity=None):
         offs.append(acc)
         acc += c
     return q, offs
+
+
+def plan_shards_mem(num_classes: int, world_size: int, capacity=None, mem_bytes=None,
+                    bytes_per_class: int = 1, fixed_bytes: int = 0):
+    """Algorithm 1, "Memory-Constraint Load Balancing", in whole classes.
+
+    Lines of Alg. 1, in order (TG_mem = C * bytes_per_class, DM_i = mem_bytes[i] - fixed_bytes,
+    DF_i = capacity[i]):
+      init (PAPER.md:947-951): load_ratios = DF_i / sum DF -> n = plan_shards (Hamilton);
+        mem_utils[i] = n_i * bpc / DM_i; flop_utils[i] = n_i / DF_i (TG_flop cancels);
+        oom_devices = {mem_util > 1}, free_devices = the rest
+      loop (PAPER.md:952-958): peak = argmax_{oom} mem_util; valley = argmin_{free}
+        (flop_util, mem_util); shift_load: move b = min(peak overload, valley headroom)
+        classes (b = "the maximum number that the valley_device will not go OOM",
+        PAPER.md:982-983, capped at the overload -- SPEC.md:418); success -> update
+        profile; else pop the valley.
+    Readings (R13): ties by lower index; the peak leaves oom_devices iff it now
+    fits; residual OOM, or a shard left with 0 classes -> PlanError(2).
+    All comparisons in exact rationals.  mem_bytes=None -> plain plan_shards.
+    """
+    from fractions import Fraction
+
+    q, _ = plan_shards(num_classes, world_size, capacity)
+    if mem_bytes is None:
+        return plan_shards(num_classes, world_size, capacity)
+    N = int(world_size)
+    w = [1] * N if capacity is None else [int(v) for v in capacity]
+    if len(mem_bytes) != N or int(bytes_per_class) <= 0:
+        raise PlanError(1, "mem_bytes needs world_size entries and bytes_per_class > 0")
+    room = [int(m) - int(fixed_bytes) for m in mem_bytes]
+    cap = [max(0, r // int(bytes_per_class)) for r in room]   # classes that fit (DM_i / bpc)
+    n = list(q)
+
+    def mem_util(i):
+        return Fraction(n[i] * int(bytes_per_class), max(room[i], 1)) if room[i] > 0 else Fraction(10 ** 30)
+
+    def flop_util(i):
+        return Fraction(n[i], w[i])
+
+    oom = [i for i in range(N) if n[i] > cap[i]]
+    free = [i for i in range(N) if n[i] <= cap[i]]
+    while oom and free:
+        peak = max(oom, key=lambda i: (mem_util(i), -i))
+        valley = min(free, key=lambda i: (flop_util(i), mem_util(i), i))
+        head = cap[valley] - n[valley]
+        if head > 0:
+            b = min(n[peak] - cap[peak], head)
+            n[peak] -= b
+            n[valley] += b
+            if n[peak] <= cap[peak]:
+                oom.remove(peak)
+        else:
+            free.remove(valley)
+    if oom:
+        raise PlanError(2, "memory-infeasible: devices %s still overloaded" % oom)
+    if any(c == 0 for c in n):
+        raise PlanError(2, "a shard would receive 0 classes")
+    offs, acc = [], 0
+    for c in n:
+        offs.append(acc)
+        acc += c
+    return n, offs

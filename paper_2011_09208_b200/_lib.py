@@ -20,7 +20,7 @@ WHALE_BF16, WHALE_F32 = 0, 1
 
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "whale_splitfc_plan", "whale_splitfc_workspace_size", "whale_splitfc_create", "whale_splitfc_forward",
+    "whale_splitfc_plan", "whale_splitfc_plan_mem", "whale_splitfc_workspace_size", "whale_splitfc_create", "whale_splitfc_forward",
     "whale_splitfc_backward", "whale_splitfc_check", "whale_splitfc_destroy", "whale_last_error",
     "whale_splitfc_launches_per_step", "whale_splitfc_profile_enable", "whale_splitfc_profile_read",
     "whale_splitfc_config",
@@ -67,6 +67,10 @@ def lib() -> ctypes.CDLL:
     L.whale_splitfc_plan.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint32),
                                      ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
     L.whale_splitfc_plan.restype = st
+    L.whale_splitfc_plan_mem.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_uint32),
+                                         ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint64, ctypes.c_uint64,
+                                         ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+    L.whale_splitfc_plan_mem.restype = st
     L.whale_splitfc_workspace_size.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ctypes.c_size_t),
                                                ctypes.POINTER(ctypes.c_size_t)]
     L.whale_splitfc_workspace_size.restype = st
@@ -111,6 +115,20 @@ def whale_splitfc_plan(num_classes: int, world_size: int, capacity=None):
     if capacity is not None:
         cap = (ctypes.c_uint32 * len(capacity))(*[int(v) for v in capacity])
     _check(L.whale_splitfc_plan(int(num_classes), int(world_size), cap, counts, offs), "whale_splitfc_plan")
+    return list(counts), list(offs)
+
+
+def whale_splitfc_plan_mem(num_classes: int, world_size: int, capacity=None, mem_bytes=None,
+                           bytes_per_class: int = 1, fixed_bytes: int = 0):
+    """Algorithm 1 plan under memory caps -> (counts, offsets); raises WhaleError."""
+    L = lib()
+    n = max(int(world_size), 1)
+    counts = (ctypes.c_int64 * n)()
+    offs = (ctypes.c_int64 * n)()
+    cap = None if capacity is None else (ctypes.c_uint32 * len(capacity))(*[int(v) for v in capacity])
+    mem = None if mem_bytes is None else (ctypes.c_uint64 * len(mem_bytes))(*[int(v) for v in mem_bytes])
+    _check(L.whale_splitfc_plan_mem(int(num_classes), int(world_size), cap, mem, int(bytes_per_class),
+                                    int(fixed_bytes), counts, offs), "whale_splitfc_plan_mem")
     return list(counts), list(offs)
 
 

@@ -82,6 +82,78 @@ extern "C" whale_status_t whale_splitfc_plan(int64_t num_classes, int32_t world_
   return WHALE_OK;
 }
 
+// ============================================================================ plan + memory (NEXT-1)
+// Algorithm 1 "Memory-Constraint Load Balancing" in whole classes,
+// starting from the proportional plan; exact rational comparisons (cross-multiplied).
+namespace {
+struct Ratio {  // num / den, den > 0
+  __int128 num, den;
+};
+inline bool lt(const Ratio& a, const Ratio& b) { return a.num * b.den < b.num * a.den; }
+inline bool eq(const Ratio& a, const Ratio& b) { return a.num * b.den == b.num * a.den; }
+}  // namespace
+
+extern "C" whale_status_t whale_splitfc_plan_mem(int64_t num_classes, int32_t world_size, const uint32_t* capacity,
+                                                 const uint64_t* mem_bytes, uint64_t bytes_per_class,
+                                                 uint64_t fixed_bytes, int64_t* shard_counts,
+                                                 int64_t* shard_offsets) {
+  whale_status_t st = whale_splitfc_plan(num_classes, world_size, capacity, shard_counts, shard_offsets);
+  if (mem_bytes == nullptr) return st;
+  if (bytes_per_class == 0) return fail(WHALE_ERR_INVALID_ARG, "bytes_per_class must be > 0");
+  if (st != WHALE_OK) return st;
+  const int N = world_size;
+  int64_t n[kMaxRanks], cap[kMaxRanks];
+  __int128 room[kMaxRanks];
+  bool in_oom[kMaxRanks], in_free[kMaxRanks];
+  for (int i = 0; i < N; ++i) {
+    n[i] = shard_counts[i];
+    room[i] = static_cast<__int128>(mem_bytes[i]) - static_cast<__int128>(fixed_bytes);
+    cap[i] = room[i] > 0 ? static_cast<int64_t>(room[i] / bytes_per_class) : 0;
+    in_oom[i] = n[i] > cap[i];
+    in_free[i] = !in_oom[i];
+  }
+  auto mem_util = [&](int i) -> Ratio {
+    if (room[i] <= 0) return Ratio{static_cast<__int128>(1) << 100, 1};
+    return Ratio{static_cast<__int128>(n[i]) * bytes_per_class, room[i]};
+  };
+  auto flop_util = [&](int i) -> Ratio { return Ratio{n[i], capacity ? capacity[i] : 1u}; };
+  for (;;) {
+    int peak = -1, valley = -1;
+    for (int i = 0; i < N; ++i)
+      if (in_oom[i] && (peak < 0 || lt(mem_util(peak), mem_util(i)))) peak = i;  // ties: lower index
+    for (int i = 0; i < N; ++i) {
+      if (!in_free[i]) continue;
+      if (valley < 0) {
+        valley = i;
+        continue;
+      }
+      const Ratio fi = flop_util(i), fv = flop_util(valley);
+      if (lt(fi, fv) || (eq(fi, fv) && lt(mem_util(i), mem_util(valley)))) valley = i;
+    }
+    if (peak < 0 || valley < 0) break;
+    const int64_t head = cap[valley] - n[valley];
+    if (head > 0) {
+      const int64_t b = std::min(n[peak] - cap[peak], head);
+      n[peak] -= b;
+      n[valley] += b;
+      if (n[peak] <= cap[peak]) in_oom[peak] = false;  // leaves oom only once it fits
+    } else {
+      in_free[valley] = false;
+    }
+  }
+  for (int i = 0; i < N; ++i)
+    if (in_oom[i]) return fail(WHALE_ERR_UNSPLITTABLE, "memory-infeasible: device %d still overloaded", i);
+  for (int i = 0; i < N; ++i)
+    if (n[i] == 0) return fail(WHALE_ERR_UNSPLITTABLE, "shard %d would receive 0 classes", i);
+  int64_t off = 0;
+  for (int i = 0; i < N; ++i) {
+    shard_counts[i] = n[i];
+    shard_offsets[i] = off;
+    off += n[i];
+  }
+  return WHALE_OK;
+}
+
 // ============================================================================ configuration
 struct GemmCfg {
   int BN = 0, bk = 64, m_blocks = 0, n_blocks = 0, splits = 1, num_kb = 0, kb_per_split = 0, num_tiles = 0;

@@ -24,7 +24,7 @@ class SplitFCSoftmaxCE:
     """
 
     def __init__(self, num_classes: int, feature_dim: int, local_batch: int, capacity=None,
-                 dtype=torch.bfloat16, group=None, device=None):
+                 dtype=torch.bfloat16, group=None, device=None, mem_bytes=None, bytes_per_class=None):
         self.C, self.D, self.B = int(num_classes), int(feature_dim), int(local_batch)
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -34,7 +34,14 @@ class SplitFCSoftmaxCE:
         else:
             self.rank, self.world = 0, 1
         self.group = group
-        self.counts, self.offsets = _lib.whale_splitfc_plan(self.C, self.world, capacity)
+        if mem_bytes is None:
+            self.counts, self.offsets = _lib.whale_splitfc_plan(self.C, self.world, capacity)
+        else:
+            # Algorithm 1 under per-device memory caps (default cost: a W row in the operand
+            # dtype + an fp32 dW row per class)
+            es = 2 if dtype == torch.bfloat16 else 4
+            bpc = bytes_per_class or self.D * (es + 4)
+            self.counts, self.offsets = _lib.whale_splitfc_plan_mem(self.C, self.world, capacity, mem_bytes, bpc)
         self.C_r, self.o_r = self.counts[self.rank], self.offsets[self.rank]
         xdt = {torch.bfloat16: _lib.WHALE_BF16, torch.float32: _lib.WHALE_F32}[dtype]
         q, _keep = _lib.make_desc(self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt)

@@ -108,3 +108,35 @@ def test_shard_plan_must_partition():
     with pytest.raises(_lib.WhaleError) as e:
         _lib.whale_splitfc_workspace_size(d)
     assert e.value.status == 1
+
+
+def test_plan_mem_golden_and_matches_oracle():
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "plan_mem_examples.json")))
+    for c in g["cases"]:
+        n, _ = _lib.whale_splitfc_plan_mem(c["C"], len(c["capacity"]), c["capacity"], c["mem_bytes"],
+                                           c["bytes_per_class"])
+        assert n == c["counts"], c["cite"]
+    for c in g["errors"]:
+        with pytest.raises(_lib.WhaleError) as e:
+            _lib.whale_splitfc_plan_mem(c["C"], len(c["capacity"]), c["capacity"], c["mem_bytes"],
+                                        c["bytes_per_class"])
+        assert e.value.status == c["code"]
+    from oracle.plan_oracle import plan_shards_mem
+    rng = np.random.default_rng(5)
+    for _ in range(5000):
+        N = int(rng.integers(1, 9))
+        C = int(rng.integers(N, 10 ** 6))
+        w = [int(v) for v in rng.integers(1, 50, N)]
+        bpc = int(rng.integers(1, 10 ** 4))
+        mem = [int(v) for v in rng.integers(0, 2 * C * bpc // N + 2, N)]
+        fixed = int(rng.integers(0, 3)) * bpc
+        try:
+            ref = plan_shards_mem(C, N, w, mem, bpc, fixed)
+        except PlanError as e:
+            with pytest.raises(_lib.WhaleError) as ee:
+                _lib.whale_splitfc_plan_mem(C, N, w, mem, bpc, fixed)
+            assert ee.value.status == e.code
+            continue
+        assert _lib.whale_splitfc_plan_mem(C, N, w, mem, bpc, fixed) == (list(ref[0]), list(ref[1]))
+    # no caps -> identical to the proportional plan
+    assert _lib.whale_splitfc_plan_mem(100000, 8, [2] + [1] * 7) == _lib.whale_splitfc_plan(100000, 8, [2] + [1] * 7)

@@ -17,6 +17,7 @@ import torch
 
 import oracle
 import oracle.splitfc_oracle
+import oracle.plan_oracle
 from oracle import PlanError, plan_shards
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
@@ -320,3 +321,45 @@ def test_sampled_oracle_agrees_with_full():
     cls = [0, 3, 49]
     np.testing.assert_allclose(oracle.splitfc_oracle.sampled_classes(X, W, y, cls, lse), f["dW"][cls],
                                rtol=1e-12, atol=1e-17)
+
+
+# ------------------------------------------------------- plan under memory caps (Alg. 1)
+def test_plan_mem_golden():
+    g = json.load(open(os.path.join(GOLDEN, "plan_mem_examples.json")))
+    for c in g["cases"]:
+        n, o = oracle.plan_oracle.plan_shards_mem(c["C"], len(c["capacity"]), c["capacity"], c["mem_bytes"],
+                                                  c["bytes_per_class"])
+        assert n == c["counts"], c["cite"]
+    for c in g["errors"]:
+        with pytest.raises(PlanError) as e:
+            oracle.plan_oracle.plan_shards_mem(c["C"], len(c["capacity"]), c["capacity"], c["mem_bytes"],
+                                               c["bytes_per_class"])
+        assert e.value.code == c["code"], c["cite"]
+
+
+def test_plan_mem_invariants_random():
+    """Feasible result => every shard fits its cap, counts sum to C, >= 1 each; when no cap
+    binds the result is exactly the proportional plan (Alg. 1's init)."""
+    rng = np.random.default_rng(41)
+    for _ in range(3000):
+        N = int(rng.integers(1, 9))
+        C = int(rng.integers(N, 5000))
+        w = [int(v) for v in rng.integers(1, 20, N)]
+        bpc = int(rng.integers(1, 100))
+        mem = [int(v) for v in rng.integers(0, 2 * C * bpc // N + 2, N)]
+        try:
+            n, o = oracle.plan_oracle.plan_shards_mem(C, N, w, mem, bpc)
+        except PlanError as e:
+            assert e.code == 2
+            # infeasible only if total capacity cannot hold C or Hamilton itself fails
+            continue
+        assert sum(n) == C and min(n) >= 1
+        assert all(ni * bpc <= mi for ni, mi in zip(n, mem))
+        big = [C * bpc] * N
+        assert oracle.plan_oracle.plan_shards_mem(C, N, w, big, bpc) == plan_shards(C, N, w)
+
+
+def test_plan_mem_infeasible_iff_total_too_small_when_init_ok():
+    """Total capacity < C classes => infeasible."""
+    with pytest.raises(PlanError):
+        oracle.plan_oracle.plan_shards_mem(10, 2, [1, 1], [4, 5], 1)
