@@ -321,6 +321,14 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   if (p.Cr > (1ll << 31) - 256 || p.D > (1ll << 31) - 256) return fail(WHALE_ERR_UNSUPPORTED, "dimension too large");
   const int vec = 16 / p.es;
   p.ldp = static_cast<int64_t>(align_up(p.Cr, vec));
+  {
+    // heterogeneity emulation (NEXT-1 experiment): WHALE_SM_LIMIT_R<rank>=n caps the SMs
+    // this rank's kernels use, making it a "slower GPU" (E8)
+    char name[32];
+    snprintf(name, sizeof(name), "WHALE_SM_LIMIT_R%d", p.rank);
+    const char* e = getenv(name);
+    if (e && atoi(e) > 0) sms = std::min(sms, atoi(e));
+  }
   p.sms = sms;
   const int kbk = kRowBytes / p.es;   // K elements per stage
   const int atom = kRowBytes / p.es;  // MN-major atom / fwd P~ chunk
