@@ -148,7 +148,10 @@ whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, whale_splitf
  *   x_local  [B x D] device; labels_local [B] int32 device; w_shard [C_r x D] device
  *   loss     device float scalar (identical bits on every rank)
  *   row_loss device [B] per-row loss of this rank's rows, or NULL
- * Saves X, y, P~ and the statistics in the workspace for the following backward.
+ * Saves y, P~ and the statistics in the workspace for the following backward; X is saved
+ * there too when world_size > 1 (the gathered batch).  At world_size 1 X is NOT copied: the
+ * backward reads x_local itself, so it must stay valid and unmodified until the matching
+ * backward has run (stream order).
  */
 whale_status_t whale_splitfc_forward(whale_splitfc_ctx* ctx, const void* x_local, const int32_t* labels_local,
                                      const void* w_shard, float* loss, float* row_loss, void* stream);
@@ -164,6 +167,24 @@ whale_status_t whale_splitfc_forward(whale_splitfc_ctx* ctx, const void* x_local
  */
 whale_status_t whale_splitfc_backward(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
                                       void* dw_shard, void* stream);
+
+/*
+ * NEXT-4 extensions: the FC bias and the predictions of Example 2
+ * (`logits = FC(features)`, `predictions = Softmax(logits)`).
+ *   bias_shard  [C_r] device, x_dtype, or NULL: logits = X W_r^T + b_r (a Dense layer with
+ *               bias; the 782 MB FC size of PAPER.md:71 suggests one, R2)
+ *   pred_local  [B] int32 device or NULL: top-1 class of each of this rank's rows (argmax of
+ *               the softmax over ALL classes; ties -> lowest class id)
+ *   prob_local  [B] float device or NULL (requires pred_local): its softmax probability
+ * whale_splitfc_forward(...) == whale_splitfc_forward_ex(..., NULL bias, ..., NULL, NULL).
+ */
+whale_status_t whale_splitfc_forward_ex(whale_splitfc_ctx* ctx, const void* x_local, const int32_t* labels_local,
+                                        const void* w_shard, const void* bias_shard, float* loss, float* row_loss,
+                                        int32_t* pred_local, float* prob_local, void* stream);
+/*   db_shard    [C_r] fp32 device or NULL: d loss / d b_r = sum over the global batch of G_r
+ * whale_splitfc_backward(...) == whale_splitfc_backward_ex(..., NULL). */
+whale_status_t whale_splitfc_backward_ex(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
+                                         void* dw_shard, float* db_shard, void* stream);
 
 /* Synchronise `stream` and surface device-detected errors (WHALE_ERR_LABEL, WHALE_ERR_COMM);
  * clears the error word. */

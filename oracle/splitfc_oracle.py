@@ -52,13 +52,18 @@ def row_stats(Z: np.ndarray):
     return m, s, m + np.log(s)
 
 
-def forward(X, W, y) -> dict:
+def forward(X, W, y, b=None) -> dict:
     """O2-O4: loss L (mean over the global batch), per-row loss and statistics.
 
     PAPER.md:287 (loss between produced and desired scores); PAPER.md:690 (Softmax under
     split).  ``y`` holds integer class ids in [0, C); out-of-range labels raise.
+    Optional FC bias b [C] (NEXT-4, reading R2): Z = X W^T + b.
+    Predictions (PAPER.md:690 ``predictions = Softmax(logits)``), top-1 form: pred_i =
+    argmax_j Z_ij (first maximum -> lowest class id), prob_i = exp(max_j Z_ij - lse_i).
     """
     Z = logits(X, W)
+    if b is not None:
+        Z = Z + _f64(b)[None, :]
     y = np.asarray(y, dtype=np.int64)
     C = Z.shape[1]
     if y.shape != (Z.shape[0],):
@@ -69,7 +74,10 @@ def forward(X, W, y) -> dict:
     zy = Z[np.arange(Z.shape[0]), y]
     row_loss = lse - zy
     loss = row_loss.mean() if Z.shape[0] else np.float64("nan")
-    return {"Z": Z, "m": m, "s": s, "lse": lse, "zy": zy, "row_loss": row_loss, "loss": loss}
+    pred = Z.argmax(axis=1) if Z.shape[0] else np.zeros(0, np.int64)
+    prob = np.exp(m - lse)
+    return {"Z": Z, "m": m, "s": s, "lse": lse, "zy": zy, "row_loss": row_loss, "loss": loss,
+            "pred": pred, "prob": prob}
 
 
 def softmax_grad(Z: np.ndarray, lse: np.ndarray, y) -> np.ndarray:
@@ -80,14 +88,15 @@ def softmax_grad(Z: np.ndarray, lse: np.ndarray, y) -> np.ndarray:
     return P / B
 
 
-def forward_backward(X, W, y) -> dict:
-    """O2-O6: loss, G, dW = G^T X, dX = G W (all float64)."""
+def forward_backward(X, W, y, b=None) -> dict:
+    """O2-O6: loss, G, dW = G^T X, dX = G W (all float64); with a bias also db = sum_i G_i."""
     Xd, Wd = _f64(X), _f64(W)
-    f = forward(Xd, Wd, y)
+    f = forward(Xd, Wd, y, b)
     G = softmax_grad(f["Z"], f["lse"], y)
     f["G"] = G
     f["dW"] = G.T @ Xd
     f["dX"] = G @ Wd
+    f["db"] = G.sum(axis=0)
     return f
 
 

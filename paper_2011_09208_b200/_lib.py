@@ -23,7 +23,7 @@ EXPORTS = (
     "whale_splitfc_plan", "whale_splitfc_plan_mem", "whale_splitfc_workspace_size", "whale_splitfc_create", "whale_splitfc_forward",
     "whale_splitfc_backward", "whale_splitfc_check", "whale_splitfc_destroy", "whale_last_error",
     "whale_splitfc_launches_per_step", "whale_splitfc_profile_enable", "whale_splitfc_profile_read",
-    "whale_splitfc_config",
+    "whale_splitfc_config", "whale_splitfc_forward_ex", "whale_splitfc_backward_ex",
 )
 
 
@@ -80,6 +80,10 @@ def lib() -> ctypes.CDLL:
     L.whale_splitfc_forward.restype = st
     L.whale_splitfc_backward.argtypes = [vp, vp, vp, vp, vp]
     L.whale_splitfc_backward.restype = st
+    L.whale_splitfc_forward_ex.argtypes = [vp] * 10
+    L.whale_splitfc_forward_ex.restype = st
+    L.whale_splitfc_backward_ex.argtypes = [vp] * 6
+    L.whale_splitfc_backward_ex.restype = st
     L.whale_splitfc_check.argtypes = [vp, vp]
     L.whale_splitfc_check.restype = st
     L.whale_splitfc_destroy.argtypes = [vp]
@@ -166,6 +170,16 @@ def whale_splitfc_forward(ctx, x_local, labels_local, w_shard, loss, row_loss, s
 
 def whale_splitfc_backward(ctx, w_shard, dx_local, dw_shard, stream):
     _check(lib().whale_splitfc_backward(ctx, w_shard, dx_local, dw_shard, stream or None), "whale_splitfc_backward")
+
+
+def whale_splitfc_forward_ex(ctx, x_local, labels_local, w_shard, bias, loss, row_loss, pred, prob, stream):
+    _check(lib().whale_splitfc_forward_ex(ctx, x_local, labels_local, w_shard, bias or None, loss, row_loss or None,
+                                          pred or None, prob or None, stream or None), "whale_splitfc_forward_ex")
+
+
+def whale_splitfc_backward_ex(ctx, w_shard, dx_local, dw_shard, db_shard, stream):
+    _check(lib().whale_splitfc_backward_ex(ctx, w_shard, dx_local, dw_shard, db_shard or None, stream or None),
+           "whale_splitfc_backward_ex")
 
 
 def whale_splitfc_check(ctx, stream):

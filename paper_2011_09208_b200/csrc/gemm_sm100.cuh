@@ -65,6 +65,8 @@ struct GemmArgs {
   float* m_tile;            // [M x n_blocks]
   float* s_tile;            // [M x n_blocks]
   float* zy;                // [M] label logit (written by the owner tile only)
+  const void* bias;         // [N] FC bias of this shard (ES-sized elements) or NULL (NEXT-4)
+  int32_t* a_tile;          // [M x n_blocks] argmax class (global id) per row and tile, or NULL
   // producer-side wait for peer data (NVLink all-gather) before the first A load
   const uint32_t* wait_flags;  // [wait_count] local flag words, NULL = no wait
   int wait_count;
@@ -476,15 +478,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const bool rv = row < a.M;
           const int ncol = min(a.BN, a.N - nb * a.BN);  // valid classes in this tile
           constexpr float kLog2e = 1.4426950408889634f;
-          // pass 1: row max over the tile's valid classes
+          // pass 1: row max (and its first column = top-1 within the tile) over valid classes
+          // FC bias (NEXT-4): every lane of a warp reads the same column -> broadcast loads
+          // through L1 (no shared-memory staging, so the stage count is unchanged)
+          const bool has_bias = a.bias != nullptr;
+          const long long bcol0 = static_cast<long long>(nb) * a.BN;
+          auto bias_at = [&](int c) -> float {
+            if (bcol0 + c >= a.N) return 0.f;
+            if constexpr (ES == 2) return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(a.bias) + bcol0 + c));
+            else return __ldg(reinterpret_cast<const float*>(a.bias) + bcol0 + c);
+          };
           float mx = -INFINITY;
+          int am = 0;
           for (int c0 = 0; c0 < a.BN; c0 += 32) {
             uint32_t v[32];
             tmem_ld32(tbase + c0, v);
             tmem_ld_wait();
 #pragma unroll
-            for (int c = 0; c < 32; ++c)
-              if (c0 + c < ncol) mx = fmaxf(mx, __uint_as_float(v[c]));
+            for (int c = 0; c < 32; ++c) {
+              const float z = __uint_as_float(v[c]) + (has_bias ? bias_at(c0 + c) : 0.f);
+              if (c0 + c < ncol && z > mx) {  // strict: ties keep the lowest class
+                mx = z;
+                am = c0 + c;
+              }
+            }
           }
           long long yl = -1;
           if (rv) yl = static_cast<long long>(a.labels[row]) - a.class_offset - static_cast<long long>(nb) * a.BN;
@@ -504,8 +521,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             uint32_t pk[32];
 #pragma unroll
             for (int c = 0; c < kChunk; c += 2) {
-              const float z0 = __uint_as_float(v[c]);
-              const float z1 = __uint_as_float(v[c + 1]);
+              const float z0 = __uint_as_float(v[c]) + (has_bias ? bias_at(c0 + c) : 0.f);
+              const float z1 = __uint_as_float(v[c + 1]) + (has_bias ? bias_at(c0 + c + 1) : 0.f);
               const float p0 = (c0 + c < ncol) ? ex2_approx(fmaf(z0, kLog2e, -mxl)) : 0.f;
               const float p1 = (c0 + c + 1 < ncol) ? ex2_approx(fmaf(z1, kLog2e, -mxl)) : 0.f;
               s += p0 + p1;
@@ -536,6 +553,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (rv) {
             a.m_tile[static_cast<size_t>(row) * a.n_blocks + nb] = mx;
             a.s_tile[static_cast<size_t>(row) * a.n_blocks + nb] = s;
+            if (a.a_tile != nullptr)
+              a.a_tile[static_cast<size_t>(row) * a.n_blocks + nb] =
+                  static_cast<int32_t>(a.class_offset + static_cast<long long>(nb) * a.BN + am);
             if (yl >= 0 && yl < ncol) a.zy[row] = zy;
           }
         }

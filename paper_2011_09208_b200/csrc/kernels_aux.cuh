@@ -122,7 +122,29 @@ struct StatsArgs {
   unsigned* counter;
   int* err;
   int grad_vecs;         // 16-byte vectors of P~ per thread in the fused gradient (chunk size)
+  // NEXT-4 predictions (optional): top-1 class of each local row and its probability
+  const int32_t* a_tile; // [Bt x T] argmax class per (row, tile) from the logits epilogue
+  int32_t* pred_local;   // [B] or NULL
+  float* prob_local;     // [B] or NULL
 };
+
+__device__ __forceinline__ int block_min_int128(int v, int* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const int r = min(min(red[0], red[1]), min(red[2], red[3]));
+  __syncthreads();
+  return r;
+}
+
+// Lowest tile index whose max equals the row max m (the row's top-1 lives there).
+__device__ __forceinline__ int argmax_tile(const float* mt, int T, float m, int* red) {
+  int tmin = 0x7fffffff;
+  for (int t = threadIdx.x; t < T; t += 128)
+    if (__ldg(mt + t) == m) tmin = min(tmin, t);
+  return block_min_int128(tmin, red);
+}
 
 constexpr int kStatsThreads = 128;
 
@@ -312,6 +334,14 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
     a.row_loss_all[i] = l - zy;
     if (a.row_loss_local) a.row_loss_local[i] = l - zy;
   }
+  if (a.pred_local != nullptr && blockIdx.x == 0) {  // top-1: first tile holding the row max
+    __shared__ int redi[4];
+    const int ts = argmax_tile(mt, a.T, m, redi);
+    if (threadIdx.x == 0) {
+      a.pred_local[i] = a.a_tile[static_cast<size_t>(i) * a.T + ts];
+      if (a.prob_local) a.prob_local[i] = 1.f / s;  // e^{m - lse}
+    }
+  }
   // ---- G for this CTA's chunk of the row
   const long long chunk = static_cast<long long>(kStatsThreads) * a.grad_vecs * V;
 #pragma unroll 4
@@ -403,6 +433,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
       s += __ldg(st + t) * __expf(__ldg(mt + t) - m);
     s = block_sum128(s, red);
     if (tslot >= 0) g_dbg_ts[tslot + 1] = gtime_ns();
+    __shared__ int redi[4];
+    const int top = argmax_tile(mt, a.T, m, redi);  // this rank's top-1 tile for the row
+    const int top_class = a.a_tile[static_cast<size_t>(i) * a.T + top];
     if (threadIdx.x < a.world) {  // thread p pushes the record to peer p
       if (threadIdx.x == 0 && (y < 0 || y >= a.C)) atomicOr(a.err, ERR_LABEL);
       const bool own = (y >= a.o_r) && (y < a.o_r + a.C_r);
@@ -414,6 +447,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
       st_relaxed_sys_v2(dst + 0, __float_as_uint(m), e);
       st_relaxed_sys_v2(dst + 1, __float_as_uint(s), e);
       st_relaxed_sys_v2(dst + 2, __float_as_uint(zy), e);
+      st_relaxed_sys_v2(dst + 3, static_cast<uint32_t>(top_class), e);
     }
     if (tslot >= 0) g_dbg_ts[tslot + 2] = gtime_ns();
   }
@@ -425,18 +459,28 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
     const float mv = __uint_as_float(wait_ll(src + 0, e, a.err, ERR_COMM));
     const float sv = __uint_as_float(wait_ll(src + 1, e, a.err, ERR_COMM));
     const float zv = __uint_as_float(wait_ll(src + 2, e, a.err, ERR_COMM));
-    recs[threadIdx.x] = make_float4(mv, sv, zv, 0.f);
+    const uint32_t cv = wait_ll(src + 3, e, a.err, ERR_COMM);
+    recs[threadIdx.x] = make_float4(mv, sv, zv, __uint_as_float(cv));
   }
   __syncthreads();
   if (tslot >= 0) g_dbg_ts[tslot + 3] = gtime_ns();
   float mm = -INFINITY;
-  for (int p = 0; p < a.world; ++p) mm = fmaxf(mm, recs[p].x);
+  int top_rank = 0;
+  for (int p = 0; p < a.world; ++p)
+    if (recs[p].x > mm) {  // strict: the lowest rank (= lowest class ids) wins ties
+      mm = recs[p].x;
+      top_rank = p;
+    }
   float ss = 0.f, zz = 0.f;
   for (int p = 0; p < a.world; ++p) {
     ss += recs[p].y * __expf(recs[p].x - mm);
     zz += recs[p].z;  // exactly one rank owns the label; the others contribute 0
   }
   const float l = mm + logf(ss);
+  if (chunk_id == 0 && threadIdx.x == 0 && a.pred_local && i >= a.rank * a.B && i < (a.rank + 1) * a.B) {
+    a.pred_local[i - a.rank * a.B] = static_cast<int32_t>(__float_as_uint(recs[top_rank].w));
+    if (a.prob_local) a.prob_local[i - a.rank * a.B] = 1.f / ss;  // e^{m - lse}
+  }
   if (chunk_id == 0 && threadIdx.x == 0) {
     a.lse[i] = l;
     a.row_loss_all[i] = l - zz;
@@ -517,6 +561,55 @@ __global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict
     } else {
       reinterpret_cast<float4*>(dx_local)[e] = acc;
     }
+  }
+}
+
+// ---------------------------------------------------------------- NEXT-4 bias gradient
+// db_r[j] = sum_i G_r[i, j] (the FC bias gradient; G already includes 1/B_tot).
+// Pass 1: grid (column vectors, 128-row chunks) -> part[chunk][j]; pass 2 sums the chunks
+// in order.  Both passes use fixed summation orders (deterministic).
+constexpr int kDbRows = 128;
+template <int ES>
+__global__ void __launch_bounds__(128) bias_grad_part_kernel(const void* G, long long ldp, int Bt, long long C_r,
+                                                             float* part /*[chunks x C_r]*/) {
+  constexpr int V = 16 / ES;
+  pdl_wait();
+  pdl_trigger();
+  const long long j0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * V;
+  if (j0 >= C_r) return;
+  const int r0 = blockIdx.y * kDbRows, r1 = min(Bt, r0 + kDbRows);
+  float acc[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) acc[k] = 0.f;
+#pragma unroll 4
+  for (int r = r0; r < r1; ++r) {
+    if constexpr (ES == 2) {
+      const uint4 raw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(G) + r * ldp + j0));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h[k]);
+        acc[2 * k] += f.x;
+        acc[2 * k + 1] += f.y;
+      }
+    } else {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G) + r * ldp + j0));
+      acc[0] += f.x; acc[1] += f.y; acc[2] += f.z; acc[3] += f.w;
+    }
+  }
+  float* o = part + static_cast<size_t>(blockIdx.y) * C_r + j0;
+#pragma unroll
+  for (int k = 0; k < V; ++k)
+    if (j0 + k < C_r) o[k] = acc[k];
+}
+__global__ void __launch_bounds__(256) bias_grad_sum_kernel(const float* part, int chunks, long long C_r, float* db) {
+  pdl_wait();
+  pdl_trigger();
+  for (long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; j < C_r;
+       j += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int c = 0; c < chunks; ++c) s += part[c * C_r + j];
+    db[j] = s;
   }
 }
 

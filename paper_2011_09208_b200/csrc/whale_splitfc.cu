@@ -182,6 +182,7 @@ static void maybe_pair(GemmCfg& g, int sms, bool b_mn, int atom) {
 struct Layout {
   // local workspace offsets
   size_t P = 0, m_tile = 0, s_tile = 0, zy = 0, lse = 0, row_loss = 0, dxpart = 0, counters = 0, tile_cnt = 0;
+  size_t a_tile = 0, dbpart = 0;  // NEXT-4: per-(row, tile) top-1 class; bias-gradient partials
   size_t local_total = 0;
   // fp32 (kind::tf32) backward only: K-major transposed operands
   size_t XT = 0, GT = 0, WT = 0;
@@ -361,6 +362,8 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   L.dxpart = take(static_cast<size_t>(p.dx.splits) * p.Bt * p.D * 4);
   L.counters = take(64 * 4);
   L.tile_cnt = take(static_cast<size_t>(p.dx.m_blocks) * p.dx.n_blocks * 4);
+  L.a_tile = take(static_cast<size_t>(p.Bt) * T * 4);
+  L.dbpart = take(static_cast<size_t>(cdiv(p.Bt, kDbRows)) * p.Cr * 4);
   if (p.es == 4) {
     L.ld_bt = static_cast<int64_t>(align_up(p.Bt, 4));
     L.XT = take(static_cast<size_t>(p.D) * L.ld_bt * 4);
@@ -460,8 +463,8 @@ struct ProfRec {
   cudaEvent_t a, b;
 };
 static const char* kKindNames[] = {"bridge_gather", "logits_gemm",  "stats_combine", "softmax_grad", "dw_gemm",
-                                   "dx_gemm",       "dx_rs_reduce", "transpose_f32", "bwd_gemm"};
-enum KernelKind { K_GATHER, K_LOGITS, K_STATS, K_GRAD, K_DW, K_DX, K_RS_REDUCE, K_TRANSPOSE, K_BWD, K_NUM };
+                                   "dx_gemm",       "dx_rs_reduce", "transpose_f32", "bwd_gemm", "bias_grad"};
+enum KernelKind { K_GATHER, K_LOGITS, K_STATS, K_GRAD, K_DW, K_DX, K_RS_REDUCE, K_TRANSPOSE, K_BWD, K_DB, K_NUM };
 
 struct whale_splitfc_ctx {
   Plan p;
@@ -723,7 +726,8 @@ static int gather_grid(const Plan& p) {
 // ============================================================================ forward
 template <int ES>
 static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, const int32_t* y_local,
-                                   const void* w, float* loss, float* row_loss, cudaStream_t s) {
+                                   const void* w, const void* bias, float* loss, float* row_loss,
+                                   int32_t* pred, float* prob, cudaStream_t s) {
   const Plan& p = c->p;
   const Layout& L = p.L;
   unsigned* counters = wsp<unsigned>(c, L.counters);
@@ -762,6 +766,8 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     GemmArgs a = base_args(p.fwd, static_cast<int>(p.Bt), static_cast<int>(p.Cr));
     a.dev_epoch = dev_epoch;
     a.labels = yg;
+    a.bias = bias;
+    a.a_tile = wsp<int32_t>(c, L.a_tile);
     a.class_offset = p.o_r;
     a.m_tile = wsp<float>(c, L.m_tile);
     a.s_tile = wsp<float>(c, L.s_tile);
@@ -808,6 +814,9 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.err = err;
     // every CTA re-reads its row's T tile partials (8T bytes): size the chunk so that this
     // stays <= ~10% of the chunk's P~ read+write traffic (4096 B per vector of the 128 threads)
+    a.a_tile = wsp<int32_t>(c, L.a_tile);
+    a.pred_local = pred;
+    a.prob_local = prob;
     a.grad_vecs = static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(4, (p.fwd.n_blocks * 10 + 511) / 512)));
     const int64_t chunk = static_cast<int64_t>(kStatsThreads) * a.grad_vecs * (16 / ES);
     if (p.world == 1) {
@@ -834,7 +843,16 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
 extern "C" whale_status_t whale_splitfc_forward(whale_splitfc_ctx* ctx, const void* x_local,
                                                 const int32_t* labels_local, const void* w_shard, float* loss,
                                                 float* row_loss, void* stream) {
+  return whale_splitfc_forward_ex(ctx, x_local, labels_local, w_shard, nullptr, loss, row_loss, nullptr, nullptr,
+                                  stream);
+}
+
+extern "C" whale_status_t whale_splitfc_forward_ex(whale_splitfc_ctx* ctx, const void* x_local,
+                                                   const int32_t* labels_local, const void* w_shard,
+                                                   const void* bias_shard, float* loss, float* row_loss,
+                                                   int32_t* pred_local, float* prob_local, void* stream) {
   if (!ctx || !x_local || !labels_local || !w_shard || !loss) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
+  if (prob_local && !pred_local) return fail(WHALE_ERR_INVALID_ARG, "prob_local requires pred_local");
   if (reinterpret_cast<uintptr_t>(x_local) % 16 || reinterpret_cast<uintptr_t>(w_shard) % 16)
     return fail(WHALE_ERR_INVALID_ARG, "x_local / w_shard must be 16-byte aligned");
   ctx->epoch += 1;
@@ -845,15 +863,17 @@ extern "C" whale_status_t whale_splitfc_forward(whale_splitfc_ctx* ctx, const vo
     whale_status_t sb = launch(ctx, epoch_bump_kernel, dim3(1), dim3(32), 0, s, dev_epoch);
     if (sb != WHALE_OK) return sb;
   }
-  whale_status_t st = ctx->p.es == 2 ? forward_impl<2>(ctx, x_local, labels_local, w_shard, loss, row_loss, s)
-                                     : forward_impl<4>(ctx, x_local, labels_local, w_shard, loss, row_loss, s);
+  whale_status_t st =
+      ctx->p.es == 2
+          ? forward_impl<2>(ctx, x_local, labels_local, w_shard, bias_shard, loss, row_loss, pred_local, prob_local, s)
+          : forward_impl<4>(ctx, x_local, labels_local, w_shard, bias_shard, loss, row_loss, pred_local, prob_local, s);
   if (st == WHALE_OK) ctx->have_fwd = true;
   return st;
 }
 
 // ============================================================================ backward
 template <int ES>
-static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* dx_local, void* dw,
+static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* dx_local, void* dw, float* db,
                                     cudaStream_t s) {
   const Plan& p = c->p;
   const Layout& L = p.L;
@@ -881,6 +901,19 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
                      p.fwd.BN, p.fwd.n_blocks, static_cast<const float*>(wsp<float>(c, L.m_tile)),
                      static_cast<const float*>(wsp<float>(c, L.lse)), yg, static_cast<long long>(p.o_r),
                      static_cast<float>(1.0 / static_cast<double>(p.Bt)))));
+  }
+  // ---- NEXT-4 bias gradient db_r = sum_i G_r[i, :] (fixed row order, two passes)
+  if (db != nullptr) {
+    constexpr int V = 16 / ES;
+    const int chunks = cdiv(p.Bt, kDbRows);
+    float* part = wsp<float>(c, L.dbpart);
+    PROFILED(K_DB, s,
+             (launch(c, bias_grad_part_kernel<ES>, dim3(cdiv(cdiv(p.Cr, V), 128), chunks), dim3(128), 0, s,
+                     static_cast<const void*>(c->ws + L.P), static_cast<long long>(p.ldp), static_cast<int>(p.Bt),
+                     static_cast<long long>(p.Cr), part)));
+    PROFILED(K_DB, s,
+             (launch(c, bias_grad_sum_kernel, dim3(std::max(1, std::min(cdiv(p.Cr, 256), 4 * p.sms))), dim3(256), 0,
+                     s, static_cast<const float*>(part), chunks, static_cast<long long>(p.Cr), db)));
   }
   // ---- A8 args: fused split-K fixup; N = 1 writes dX, N > 1 pushes rows to their owners
   GemmArgs ax = base_args(p.dx, static_cast<int>(p.Bt), static_cast<int>(p.D));
@@ -983,13 +1016,18 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
 
 extern "C" whale_status_t whale_splitfc_backward(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
                                                  void* dw_shard, void* stream) {
+  return whale_splitfc_backward_ex(ctx, w_shard, dx_local, dw_shard, nullptr, stream);
+}
+
+extern "C" whale_status_t whale_splitfc_backward_ex(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
+                                                    void* dw_shard, float* db_shard, void* stream) {
   if (!ctx || !w_shard || !dx_local || !dw_shard) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
   if (!ctx->have_fwd) return fail(WHALE_ERR_STATE, "backward called before forward");
   if (reinterpret_cast<uintptr_t>(dx_local) % 16 || reinterpret_cast<uintptr_t>(dw_shard) % 16)
     return fail(WHALE_ERR_INVALID_ARG, "dx_local / dw_shard must be 16-byte aligned");
   auto s = static_cast<cudaStream_t>(stream);
-  whale_status_t st = ctx->p.es == 2 ? backward_impl<2>(ctx, w_shard, dx_local, dw_shard, s)
-                                     : backward_impl<4>(ctx, w_shard, dx_local, dw_shard, s);
+  whale_status_t st = ctx->p.es == 2 ? backward_impl<2>(ctx, w_shard, dx_local, dw_shard, db_shard, s)
+                                     : backward_impl<4>(ctx, w_shard, dx_local, dw_shard, db_shard, s);
   if (st == WHALE_OK) ctx->have_fwd = false;
   return st;
 }

@@ -65,29 +65,46 @@ class SplitFCSoftmaxCE:
         self.ctx = _lib.whale_splitfc_create(self._desc)
         self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.row_loss = torch.zeros(self.B, dtype=torch.float32, device=self.device)
+        self.pred = torch.zeros(self.B, dtype=torch.int32, device=self.device)
+        self.prob = torch.zeros(self.B, dtype=torch.float32, device=self.device)
 
     # ------------------------------------------------------------------ C-ABI calls
     def forward(self, x_local: torch.Tensor, labels_local: torch.Tensor, w_shard: torch.Tensor,
-                row_loss: bool = False) -> torch.Tensor:
-        """-> device scalar loss (mean over the global batch).  labels: int32 (int64 is cast)."""
+                row_loss: bool = False, bias: torch.Tensor | None = None, predictions: bool = False):
+        """-> device scalar loss (mean over the global batch).  labels: int32 (int64 is cast).
+
+        bias: optional [C_r] FC bias shard (same dtype as W).  predictions=True also fills
+        self.pred [B] (top-1 class over all C classes) and self.prob [B] (its probability).
+        """
         self._check_inputs(x_local, w_shard)
         if labels_local.dtype != torch.int32:
             labels_local = labels_local.to(torch.int32)
         self._labels = labels_local.contiguous()  # keep alive until the kernels ran
+        self._x = x_local  # world 1: the backward reads x_local in place (header contract)
+        if bias is not None and (bias.shape != (self.C_r,) or bias.dtype != self.dtype or not bias.is_contiguous()):
+            raise ValueError(f"bias must be contiguous {self.dtype} [{self.C_r}]")
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.whale_splitfc_forward(self.ctx, x_local.data_ptr(), self._labels.data_ptr(), w_shard.data_ptr(),
-                                   self.loss.data_ptr(), self.row_loss.data_ptr() if row_loss else None, stream)
+        _lib.whale_splitfc_forward_ex(self.ctx, x_local.data_ptr(), self._labels.data_ptr(), w_shard.data_ptr(),
+                                      bias.data_ptr() if bias is not None else None, self.loss.data_ptr(),
+                                      self.row_loss.data_ptr() if row_loss else None,
+                                      self.pred.data_ptr() if predictions else None,
+                                      self.prob.data_ptr() if predictions else None, stream)
         return self.loss
 
     def backward(self, w_shard: torch.Tensor, dx_local: torch.Tensor | None = None,
-                 dw_shard: torch.Tensor | None = None):
-        """-> (dX_r [B x D] in the operand dtype, dW_r [C_r x D] fp32)."""
+                 dw_shard: torch.Tensor | None = None, db_shard: torch.Tensor | None = None, bias_grad: bool = False):
+        """-> (dX_r [B x D] in the operand dtype, dW_r [C_r x D] fp32[, db_r [C_r] fp32 if bias_grad])."""
         if dx_local is None:
             dx_local = torch.empty(self.B, self.D, dtype=self.dtype, device=self.device)
         if dw_shard is None:
             dw_shard = torch.empty(self.C_r, self.D, dtype=torch.float32, device=self.device)
+        if bias_grad and db_shard is None:
+            db_shard = torch.empty(self.C_r, dtype=torch.float32, device=self.device)
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.whale_splitfc_backward(self.ctx, w_shard.data_ptr(), dx_local.data_ptr(), dw_shard.data_ptr(), stream)
+        _lib.whale_splitfc_backward_ex(self.ctx, w_shard.data_ptr(), dx_local.data_ptr(), dw_shard.data_ptr(),
+                                       db_shard.data_ptr() if db_shard is not None else None, stream)
+        if db_shard is not None:
+            return dx_local, dw_shard, db_shard
         return dx_local, dw_shard
 
     def check(self):

@@ -25,22 +25,25 @@ def fro(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf16", seed=1, steps=2):
+def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf16", seed=1, steps=2, bias=False):
     Bt = B * world
     X = syn.gen_features((0, Bt), D, seed, dtype)
     W = syn.gen_weight((0, C), D, seed, regime, dtype)
     y = syn.gen_labels((0, Bt), C, seed)
+    bfull = syn.gen_bias((0, C), seed, 2.0, dtype) if bias else None
     op = SplitFCSoftmaxCE(C, D, B, capacity=capacity, dtype=syn.torch_dtype(dtype), group=dist.group.WORLD, device=dev)
     o, c = op.o_r, op.C_r
     xr = X[rank * B:(rank + 1) * B].to(dev)
     yr = y[rank * B:(rank + 1) * B].to(dev)
     wr = W[o:o + c].to(dev).contiguous()
-    for _ in range(steps):  # repeated steps exercise the epoch / parity double buffering
-        loss = op.forward(xr, yr, wr, row_loss=True).clone()
-        dx, dw = op.backward(wr)
+    br = bfull[o:o + c].to(dev).contiguous() if bias else None
+    for _ in range(steps):  # repeated steps exercise the device epoch / flag protocol
+        loss = op.forward(xr, yr, wr, row_loss=True, bias=br, predictions=bias).clone()
+        out = op.backward(wr, bias_grad=bias)
+        dx, dw = out[0], out[1]
     op.check()
     torch.cuda.synchronize(dev)
-    f = oracle.forward_backward(X, W, y.numpy())
+    f = oracle.forward_backward(X, W, y.numpy(), bfull)
     losses = [torch.zeros((), device=dev) for _ in range(world)]
     dist.all_gather(losses, loss)
     bit_equal = all(torch.equal(l, losses[0]) for l in losses)
@@ -54,6 +57,15 @@ def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf1
         "loss_bit_equal": bool(bit_equal),
     }
     ok = res["loss_rel"] <= 1e-3 and res["dx_rel"] <= 1e-2 and res["dw_rel"] <= 1e-2 and bit_equal
+    if bias:
+        rows = slice(rank * B, (rank + 1) * B)
+        Zs = np.sort(f["Z"][rows], axis=1)
+        clear = (Zs[:, -1] - Zs[:, -2]) > 1e-3
+        pred = op.pred.cpu().numpy()
+        res["db_rel"] = fro(out[2].cpu(), f["db"][o:o + c])
+        res["pred_ok"] = bool(np.array_equal(pred[clear], f["pred"][rows][clear]))
+        res["prob_rel"] = float(np.max(np.abs(op.prob.cpu().numpy() - f["prob"][rows]) / f["prob"][rows]))
+        ok = ok and res["db_rel"] <= 1e-2 and res["pred_ok"] and res["prob_rel"] <= 1e-3
     res["ok"] = ok
     allres = [None] * world
     dist.all_gather_object(allres, res)
@@ -74,6 +86,7 @@ def main():
         dict(B=32, D=256, C=5000, capacity=[2] + [1] * (world - 1)),  # uneven (c3-like)
         dict(B=64, D=520, C=20000),
         dict(B=32, D=2048, C=100_000),                              # c2 shape
+        dict(B=24, D=256, C=7001, regime="peaked", bias=True),      # NEXT-4: bias, db, predictions
     ]
     ok = True
     for cs in cases:

@@ -117,3 +117,16 @@ def gen_labels(rows: tuple[int, int], C: int, seed: int, device="cpu") -> torch.
         return torch.empty(0, dtype=torch.int64, device=device)
     return _rows(seed, _STREAM_Y, a, b,
                  lambda g, n: torch.randint(0, C, (n,), generator=g, device=device), device).contiguous()
+
+
+_STREAM_B = 4
+
+
+def gen_bias(rows: tuple[int, int], seed: int, scale: float = 1.0, dtype: str = "bf16", device="cpu") -> torch.Tensor:
+    """FC bias entries for classes [a, b): N(0, scale^2) rounded to ``dtype`` (NEXT-4 tests)."""
+    a, b = rows
+    if b <= a:
+        return torch.empty(0, dtype=torch_dtype(dtype), device=device)
+    v = _rows(seed, _STREAM_B, a, b,
+              lambda g, n: torch.randn(n, generator=g, device=device, dtype=torch.float32) * scale, device)
+    return v.to(torch_dtype(dtype)).contiguous()

@@ -237,3 +237,32 @@ def test_parity_large_sampled(whale, name):
     # property at any size: column sums of dW over all classes vanish (rows of G sum to 0)
     colsum = dw.double().sum(0)
     assert float(colsum.abs().max()) <= 1e-2 * float(dw.double().abs().sum(0).max())
+
+
+# ------------------------------------------------------------ bias + predictions (NEXT-4)
+@pytest.mark.parametrize("B,D,C,dtype", [(40, 192, 1000, "bf16"), (200, 520, 3001, "bf16"),
+                                         (32, 2048, 100_000, "bf16"), (16, 64, 1000, "f32")])
+def test_bias_and_predictions(whale, B, D, C, dtype):
+    seed = 200 + B
+    X = syn.gen_features((0, B), D, seed, dtype)
+    W = syn.gen_weight((0, C), D, seed, "peaked", dtype)
+    b = syn.gen_bias((0, C), seed, 2.0, dtype)
+    y = syn.gen_labels((0, B), C, seed)
+    op = whale.SplitFCSoftmaxCE(C, D, B, dtype=syn.torch_dtype(dtype))
+    xd, wd, bd = X.cuda(), W.cuda(), b.cuda()  # x stays alive: backward reads it (header contract)
+    loss = float(op.forward(xd, y.cuda(), wd, row_loss=True, bias=bd, predictions=True))
+    dx, dw, db = op.backward(wd, bias_grad=True)
+    op.check()
+    f = oracle.forward_backward(X, W, y.numpy(), b)
+    assert abs(loss - f["loss"]) <= LOSS_RTOL * abs(f["loss"])
+    assert _fro(dx.float().cpu(), f["dX"]) <= FRO_RTOL
+    assert _fro(dw.cpu(), f["dW"]) <= FRO_RTOL
+    assert _fro(db.cpu(), f["db"]) <= FRO_RTOL
+    pred = op.pred.cpu().numpy()
+    prob = op.prob.cpu().numpy()
+    # top-1 is unique where the oracle's best and second-best logits differ clearly
+    Z = np.sort(f["Z"], axis=1)
+    clear = (Z[:, -1] - Z[:, -2]) > (2e-2 if dtype == "f32" else 1e-3)
+    assert np.array_equal(pred[clear], f["pred"][clear])
+    assert np.all((pred >= 0) & (pred < C))
+    np.testing.assert_allclose(prob, f["prob"], rtol=5e-3 if dtype == "f32" else 1e-3)

@@ -363,3 +363,36 @@ def test_plan_mem_infeasible_iff_total_too_small_when_init_ok():
     """Total capacity < C classes => infeasible."""
     with pytest.raises(PlanError):
         oracle.plan_oracle.plan_shards_mem(10, 2, [1, 1], [4, 5], 1)
+
+
+# ------------------------------------------------------------ bias + predictions (NEXT-4)
+def test_bias_against_torch_linear_fp64():
+    """Dense layer with bias: torch F.linear + cross_entropy + autograd (fp64) pins loss,
+    dX, dW and db = sum_i G_i; a constant added to every bias leaves L unchanged."""
+    B, D, C = 20, 9, 41
+    X, W, y = _rand(B, D, C, 50, scale=6.0)
+    b = np.random.default_rng(51).standard_normal(C) * 2
+    f = oracle.forward_backward(X, W, y, b)
+    Xt, Wt, bt = (torch.tensor(v, requires_grad=True) for v in (X, W, b))
+    L = torch.nn.functional.cross_entropy(torch.nn.functional.linear(Xt, Wt, bt), torch.tensor(y))
+    L.backward()
+    assert abs(f["loss"] - L.item()) <= 1e-12 * abs(L.item())
+    np.testing.assert_allclose(f["dX"], Xt.grad.numpy(), rtol=1e-10, atol=1e-15)
+    np.testing.assert_allclose(f["dW"], Wt.grad.numpy(), rtol=1e-10, atol=1e-15)
+    np.testing.assert_allclose(f["db"], bt.grad.numpy(), rtol=1e-10, atol=1e-16)
+    g = oracle.forward_backward(X, W, y, b + 3.25)
+    assert abs(g["loss"] - f["loss"]) < 1e-13
+
+
+def test_predictions_definition():
+    """pred = torch.argmax of the logits (first max), prob = softmax at pred (torch)."""
+    X, W, y = _rand(30, 7, 19, 52, scale=5.0)
+    b = np.random.default_rng(53).standard_normal(19)
+    f = oracle.forward(X, W, y, b)
+    Zt = torch.tensor(X) @ torch.tensor(W).T + torch.tensor(b)
+    P = torch.softmax(Zt, 1)
+    assert np.array_equal(f["pred"], torch.argmax(Zt, 1).numpy())
+    np.testing.assert_allclose(f["prob"], P.max(1).values.numpy(), rtol=1e-13)
+    # ties go to the lowest class id
+    Xe, We = np.eye(2), np.array([[1.0, 0.0], [1.0, 0.0], [0.0, 1.0]])
+    assert list(oracle.forward(Xe, We, [0, 2])["pred"]) == [0, 2]
