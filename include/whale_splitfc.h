@@ -115,7 +115,7 @@ whale_status_t whale_splitfc_plan_mem(int64_t num_classes, int32_t world_size, c
 typedef struct whale_splitfc_desc {
   int32_t rank;
   int32_t world_size;
-  int64_t local_batch; /* B, equal on every rank */
+  int64_t local_batch; /* B = B_rank, this rank's DP rows (must equal batch_counts[rank] if given) */
   int64_t feature_dim; /* D, multiple of 8 */
   int64_t num_classes; /* C */
   const int64_t* shard_counts;  /* [world] from whale_splitfc_plan (host memory) */
@@ -126,6 +126,12 @@ typedef struct whale_splitfc_desc {
   size_t symm_bytes;
   void* local_workspace; /* device, 256-byte aligned */
   size_t local_workspace_bytes;
+  /* NEXT-3 (hardware-aware replicate): per-rank DP batch
+   * [world] (host memory, identical on every rank), or NULL = local_batch on every rank.
+   * Rank r's rows are rows [B_0 + ... + B_{r-1}, ... + B_r) of the gathered batch (rank
+   * order); B_r may be 0 when world > 1 (that rank then only serves its class shard);
+   * sum B_r >= 1.  whale_splitfc_plan(B_tot, world, capacity) gives the proportional split. */
+  const int64_t* batch_counts;
 } whale_splitfc_desc;
 
 typedef struct whale_splitfc_ctx whale_splitfc_ctx;

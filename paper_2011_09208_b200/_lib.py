@@ -48,6 +48,7 @@ class Desc(ctypes.Structure):
         ("symm_bytes", ctypes.c_size_t),
         ("local_workspace", ctypes.c_void_p),
         ("local_workspace_bytes", ctypes.c_size_t),
+        ("batch_counts", ctypes.POINTER(ctypes.c_int64)),
     ]
 
 
@@ -137,17 +138,19 @@ def whale_splitfc_plan_mem(num_classes: int, world_size: int, capacity=None, mem
 
 
 def make_desc(rank, world, B, D, C, counts, offsets, x_dtype=WHALE_BF16, peer_ptrs=None, symm_bytes=0,
-              workspace_ptr=0, workspace_bytes=0):
-    """Build a Desc; the returned tuple keeps the ctypes arrays alive."""
+              workspace_ptr=0, workspace_bytes=0, batch_counts=None):
+    """Build a Desc; the returned tuple keeps the ctypes arrays alive.  batch_counts: optional
+    per-rank DP batch [world] (NEXT-3); B must then be batch_counts[rank]."""
     c_counts = (ctypes.c_int64 * world)(*counts)
     c_offs = (ctypes.c_int64 * world)(*offsets)
     c_peers = None
     if peer_ptrs is not None:
         c_peers = (ctypes.c_void_p * world)(*peer_ptrs)
+    c_batch = (ctypes.c_int64 * world)(*batch_counts) if batch_counts is not None else None
     d = Desc(rank, world, B, D, C, c_counts, c_offs, x_dtype, WHALE_F32,
              ctypes.cast(c_peers, ctypes.POINTER(ctypes.c_void_p)) if c_peers is not None else None,
-             symm_bytes, workspace_ptr or None, workspace_bytes)
-    return d, (c_counts, c_offs, c_peers)
+             symm_bytes, workspace_ptr or None, workspace_bytes, c_batch)
+    return d, (c_counts, c_offs, c_peers, c_batch)
 
 
 def whale_splitfc_workspace_size(desc: Desc):

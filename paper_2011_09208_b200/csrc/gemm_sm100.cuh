@@ -81,8 +81,9 @@ struct GemmArgs {
   uint32_t* tile_cnt;       // [m_blocks x n_blocks] monotonic arrival counters
   uint32_t* done_cnt;       // monotonic end-of-kernel ticket (CTAs)
   void* out;                // FIX_LOCAL: final dX [M x N] (ES-sized elements)
-  int B, rank, world;       // FIX_PUSH: rows r*B..(r+1)*B belong to rank r
-  PeerPtrs recv;            // FIX_PUSH: owner's fp32 slab [world][B x N] (this parity)
+  int B, rank, world;       // FIX_PUSH: B = slab rows per source rank (B_max)
+  int row_off[kMaxRanks + 1];  // FIX_PUSH: rows [row_off[r], row_off[r+1]) belong to rank r
+  PeerPtrs recv;            // FIX_PUSH: owner's fp32 slab [world][B x N]
   PeerFlags rs_flags;       // FIX_PUSH: &flag[RS][rank] on every rank
   int store_mode;           // EPI_STORE_F32: 0 per-warp TMA box, 1 CTA-wide TMA box, 2 st.global
   int n_fastest;            // tile order: 0 = M fastest (share B), 1 = N fastest (share A)
@@ -192,9 +193,12 @@ __device__ __forceinline__ void fixup_share(const GemmArgs& a, int mb, int nb, i
         *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + static_cast<size_t>(r) * a.N + c) = acc;
       }
     } else {
-      const int owner = r / a.B;
+      int owner = 0;  // the last rank whose rows start at or before r (empty ranks are skipped)
+#pragma unroll
+      for (int q = 1; q < kMaxRanks; ++q)
+        if (q < a.world && a.row_off[q] <= r) owner = q;
       float* dst = reinterpret_cast<float*>(a.recv.p[owner]) +
-                   (static_cast<size_t>(a.rank) * a.B + (r - owner * a.B)) * a.N + c;
+                   (static_cast<size_t>(a.rank) * a.B + (r - a.row_off[owner])) * a.N + c;
       *reinterpret_cast<float4*>(dst) = acc;  // NVLink store into the owner's slab
     }
   }

@@ -60,10 +60,12 @@ __device__ __forceinline__ bool last_of_n(unsigned* counter, unsigned n) {
 }
 
 // ---------------------------------------------------------------- A2 bridge gather
-// Rank r writes its B rows at row offset r*B of every rank's gathered X buffer, and its
-// labels likewise; the last block then raises flag[GATHER][r] = epoch on every peer.
+// Rank r writes its B_r rows at row offset R_r = B_0 + ... + B_{r-1} of every rank's gathered
+// X buffer (the concatenation in rank order), and its labels likewise; every block then
+// raises flag[GATHER][r] on every peer (B_r may be 0: the blocks still signal).
 __global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const int32_t* __restrict__ y_local,
-                                     int64_t x_vecs /*B*row_bytes/16*/, int B, int rank, int world,
+                                     int64_t x_vecs /*B_r*row_bytes/16*/, int B, int row_off /*R_r*/,
+                                     int64_t row_vecs /*row_bytes/16*/, int rank, int world,
                                      PeerPtrs dst_x /*slab base on each rank*/, PeerPtrs dst_y,
                                      PeerFlags flags /*&flag[GATHER][rank] on each rank*/, uint32_t epoch,
                                      int dbg) {
@@ -74,7 +76,7 @@ __global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const in
   pdl_trigger();
   TraceScope _trace(0);
   if (ts) g_dbg_ts[tso + 1] = globaltimer();
-  const int64_t off_vec = static_cast<int64_t>(rank) * x_vecs;
+  const int64_t off_vec = static_cast<int64_t>(row_off) * row_vecs;
   for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < x_vecs;
        v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint4 val = __ldg(x_local + v);
@@ -86,7 +88,7 @@ __global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const in
     const int32_t y = y_local[i];
 #pragma unroll
     for (int p = 0; p < kMaxRanks; ++p)
-      if (p < world) reinterpret_cast<int32_t*>(dst_y.p[p])[rank * B + i] = y;
+      if (p < world) reinterpret_cast<int32_t*>(dst_y.p[p])[row_off + i] = y;
   }
   // every block signals every peer itself (no last-block ticket): after the CTA barrier,
   // one fence.sc.sys + a release increment per peer; peers wait for epoch * gridDim.x.
@@ -109,6 +111,7 @@ struct StatsArgs {
   const float* zy_r;     // [Bt]
   const int32_t* y;      // [Bt] labels (global ids) of the gathered batch
   int T, Bt, B, rank, world;
+  int row0;              // this rank's first row in the gathered batch (R_r); its rows: [row0, row0 + B)
   long long o_r, C_r, C;
   PeerPtrs peer_stats;   // float4 [world x Bt] slab on each rank (this parity)
   PeerFlags peer_flags;  // &flag[STATS][rank] on each rank
@@ -228,7 +231,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_rows_kernel(const StatsAr
       const float l = mm + logf(ss);
       a.lse[r] = l;
       a.row_loss_all[r] = l - zz;
-      if (a.row_loss_local && r >= a.rank * a.B && r < (a.rank + 1) * a.B) a.row_loss_local[r - a.rank * a.B] = l - zz;
+      if (a.row_loss_local && r >= a.row0 && r < a.row0 + a.B) a.row_loss_local[r - a.row0] = l - zz;
     }
     __syncthreads();
   }
@@ -477,14 +480,14 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
     zz += recs[p].z;  // exactly one rank owns the label; the others contribute 0
   }
   const float l = mm + logf(ss);
-  if (chunk_id == 0 && threadIdx.x == 0 && a.pred_local && i >= a.rank * a.B && i < (a.rank + 1) * a.B) {
-    a.pred_local[i - a.rank * a.B] = static_cast<int32_t>(__float_as_uint(recs[top_rank].w));
-    if (a.prob_local) a.prob_local[i - a.rank * a.B] = 1.f / ss;  // e^{m - lse}
+  if (chunk_id == 0 && threadIdx.x == 0 && a.pred_local && i >= a.row0 && i < a.row0 + a.B) {
+    a.pred_local[i - a.row0] = static_cast<int32_t>(__float_as_uint(recs[top_rank].w));
+    if (a.prob_local) a.prob_local[i - a.row0] = 1.f / ss;  // e^{m - lse}
   }
   if (chunk_id == 0 && threadIdx.x == 0) {
     a.lse[i] = l;
     a.row_loss_all[i] = l - zz;
-    if (a.row_loss_local && i >= a.rank * a.B && i < (a.rank + 1) * a.B) a.row_loss_local[i - a.rank * a.B] = l - zz;
+    if (a.row_loss_local && i >= a.row0 && i < a.row0 + a.B) a.row_loss_local[i - a.row0] = l - zz;
   }
   // ---- G for this CTA's chunk of the row
   const long long chunk = static_cast<long long>(kStatsThreads) * a.grad_vecs * V;
@@ -530,10 +533,11 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
 }
 
 // ---------------------------------------------------------------- A8 dX reduce-scatter (owner)
-// The dX GEMM's fixup pushed every peer's reduced rows into recv[p][B x D] and raised
-// flag[RS][p]; wait for all, then dX_r = sum_p recv[p] in rank order.
+// The dX GEMM's fixup pushed every peer's reduced rows into recv[p][B_r x D] (slabs of
+// B_max rows) and raised flag[RS][p]; wait for all, then dX_r = sum_p recv[p] in rank order.
 template <int ES>
-__global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict__ recv, int B, int D, int world,
+__global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict__ recv, int B, int B_slab, int D,
+                                                        int world,
                                                         const uint32_t* my_flags, const uint32_t* dev_epoch,
                                                         void* dx_local, int* err) {
   pdl_wait();
@@ -545,11 +549,12 @@ __global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict
   __syncthreads();
   __threadfence_system();
   const int64_t total = static_cast<int64_t>(B) * (D / 4);
+  const int64_t slab = static_cast<int64_t>(B_slab) * (D / 4);
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float4 acc = __ldcg(recv + e);
     for (int p = 1; p < world; ++p) {
-      const float4 v = __ldcg(recv + p * total + e);
+      const float4 v = __ldcg(recv + p * slab + e);
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
     if constexpr (ES == 2) {

@@ -199,6 +199,8 @@ enum CounterIdx { CNT_GATHER = 0, CNT_STATS = 1, CNT_DONE = 2, CNT_SCHED = 3, CN
 struct Plan {
   int rank = 0, world = 1, es = 2;
   int64_t B = 0, Bt = 0, D = 0, C = 0, Cr = 0, o_r = 0, ldp = 0;
+  int64_t Bmax = 0;                  // largest per-rank batch (dX receive slab rows)
+  int64_t Boff[kMaxRanks + 1] = {};  // rank r's rows: [Boff[r], Boff[r+1]) of the gathered batch
   int sms = 148;
   GemmCfg fwd, dw, dx;
   Layout L;
@@ -296,8 +298,8 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   if (d->world_size < 1 || d->world_size > kMaxRanks)
     return fail(WHALE_ERR_UNSUPPORTED, "world_size %d outside [1, %d]", d->world_size, kMaxRanks);
   if (d->rank < 0 || d->rank >= d->world_size) return fail(WHALE_ERR_INVALID_ARG, "rank out of range");
-  if (d->local_batch < 1 || d->feature_dim < 1 || d->num_classes < 1)
-    return fail(WHALE_ERR_INVALID_ARG, "B, D and C must be >= 1");
+  if (d->local_batch < 0 || d->feature_dim < 1 || d->num_classes < 1)
+    return fail(WHALE_ERR_INVALID_ARG, "B >= 0, D >= 1 and C >= 1 required");
   if (d->feature_dim % 8 != 0) return fail(WHALE_ERR_UNSUPPORTED, "feature_dim %% 8 != 0 (TMA 16-byte rows)");
   if (d->x_dtype != WHALE_BF16 && d->x_dtype != WHALE_F32) return fail(WHALE_ERR_UNSUPPORTED, "x_dtype");
   if (d->dw_dtype != WHALE_F32) return fail(WHALE_ERR_UNSUPPORTED, "dw_dtype must be WHALE_F32");
@@ -313,7 +315,17 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   p.world = d->world_size;
   p.es = d->x_dtype == WHALE_BF16 ? 2 : 4;
   p.B = d->local_batch;
-  p.Bt = p.B * p.world;
+  p.Boff[0] = 0;
+  for (int r = 0; r < p.world; ++r) {
+    const int64_t br = d->batch_counts ? d->batch_counts[r] : d->local_batch;
+    if (br < 0 || br > 65535) return fail(WHALE_ERR_INVALID_ARG, "batch_counts[%d] = %lld outside [0, 65535]", r, (long long)br);
+    p.Boff[r + 1] = p.Boff[r] + br;
+    p.Bmax = std::max(p.Bmax, br);
+  }
+  if (d->batch_counts && d->batch_counts[p.rank] != d->local_batch)
+    return fail(WHALE_ERR_INVALID_ARG, "local_batch != batch_counts[rank]");
+  p.Bt = p.Boff[p.world];
+  if (p.Bt < 1 || (p.world == 1 && p.B < 1)) return fail(WHALE_ERR_INVALID_ARG, "empty global batch");
   p.D = d->feature_dim;
   p.C = d->num_classes;
   p.Cr = d->shard_counts[p.rank];
@@ -378,7 +390,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
     L.xg = take(static_cast<size_t>(p.Bt) * p.D * p.es);
     L.yg = take(p.Bt * 4);
     L.stats = take(static_cast<size_t>(p.world) * p.Bt * 32);  // LL words {m,s,zy,-} x {data, epoch}
-    L.dxrecv = take(static_cast<size_t>(p.world) * p.B * p.D * 4);
+    L.dxrecv = take(static_cast<size_t>(p.world) * p.Bmax * p.D * 4);
   }
   L.symm_total = o;
   return WHALE_OK;
@@ -716,10 +728,10 @@ static whale_status_t ensure_x_maps(whale_splitfc_ctx* c, const void* x) {
   return WHALE_OK;
 }
 
-// Blocks of the bridge gather: identical on every rank (depends on B, D only); each block
-// raises the peers' GATHER counters once, so the consumer waits for epoch * grid.
+// Blocks of the bridge gather: identical on every rank (depends on B_max, D only); each
+// block raises the peers' GATHER counters once, so the consumer waits for epoch * grid.
 static int gather_grid(const Plan& p) {
-  const int64_t x_vecs = p.B * p.D * p.es / 16;
+  const int64_t x_vecs = p.Bmax * p.D * p.es / 16;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(x_vecs, 256), 64)));
 }
 
@@ -758,7 +770,8 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     const int grid = gather_grid(p);
     PROFILED(K_GATHER, s,
              (launch(c, bridge_gather_kernel, dim3(grid), dim3(256), 0, s, static_cast<const uint4*>(x_local),
-                     y_local, x_vecs, static_cast<int>(p.B), p.rank, p.world, dx, dy, fl, 0u,
+                     y_local, x_vecs, static_cast<int>(p.B), static_cast<int>(p.Boff[p.rank]),
+                     static_cast<int64_t>(p.D * ES / 16), p.rank, p.world, dx, dy, fl, 0u,
                      env_int("WHALE_GATHER_DBG", 0))));
   }
   // ---- A3 logits GEMM with fused row statistics
@@ -792,6 +805,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.T = p.fwd.n_blocks;
     a.Bt = static_cast<int>(p.Bt);
     a.B = static_cast<int>(p.B);
+    a.row0 = static_cast<int>(p.Boff[p.rank]);
     a.rank = p.rank;
     a.world = p.world;
     a.o_r = p.o_r;
@@ -851,7 +865,8 @@ extern "C" whale_status_t whale_splitfc_forward_ex(whale_splitfc_ctx* ctx, const
                                                    const int32_t* labels_local, const void* w_shard,
                                                    const void* bias_shard, float* loss, float* row_loss,
                                                    int32_t* pred_local, float* prob_local, void* stream) {
-  if (!ctx || !x_local || !labels_local || !w_shard || !loss) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
+  if (!ctx || !w_shard || !loss) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
+  if (ctx->p.B > 0 && (!x_local || !labels_local)) return fail(WHALE_ERR_INVALID_ARG, "NULL x_local / labels_local");
   if (prob_local && !pred_local) return fail(WHALE_ERR_INVALID_ARG, "prob_local requires pred_local");
   if (reinterpret_cast<uintptr_t>(x_local) % 16 || reinterpret_cast<uintptr_t>(w_shard) % 16)
     return fail(WHALE_ERR_INVALID_ARG, "x_local / w_shard must be 16-byte aligned");
@@ -924,7 +939,8 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
   ax.done_cnt = counters + CNT_DONE;
   ax.dev_epoch = dev_epoch;
   ax.bump_epoch = 1;  // the dX launch (or the fused launch) ends the step
-  ax.B = static_cast<int>(p.B);
+  ax.B = static_cast<int>(p.Bmax);
+  for (int r = 0; r <= p.world; ++r) ax.row_off[r] = static_cast<int>(p.Boff[r]);
   ax.rank = p.rank;
   ax.world = p.world;
   if (p.world == 1) {
@@ -1008,7 +1024,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     PROFILED(K_RS_REDUCE, s,
              (launch(c, dx_reduce_kernel<ES>, dim3(g2), dim3(256), 0, s,
                      reinterpret_cast<const float4*>(c->symm[p.rank] + L.dxrecv), static_cast<int>(p.B),
-                     static_cast<int>(p.D), p.world, my_flags, static_cast<const uint32_t*>(dev_epoch), dx_local,
+                     static_cast<int>(p.Bmax), static_cast<int>(p.D), p.world, my_flags, static_cast<const uint32_t*>(dev_epoch), dx_local,
                      err)));
   }
   return WHALE_OK;
@@ -1021,7 +1037,8 @@ extern "C" whale_status_t whale_splitfc_backward(whale_splitfc_ctx* ctx, const v
 
 extern "C" whale_status_t whale_splitfc_backward_ex(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
                                                     void* dw_shard, float* db_shard, void* stream) {
-  if (!ctx || !w_shard || !dx_local || !dw_shard) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
+  if (!ctx || !w_shard || !dw_shard) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
+  if (ctx->p.B > 0 && !dx_local) return fail(WHALE_ERR_INVALID_ARG, "NULL dx_local");
   if (!ctx->have_fwd) return fail(WHALE_ERR_STATE, "backward called before forward");
   if (reinterpret_cast<uintptr_t>(dx_local) % 16 || reinterpret_cast<uintptr_t>(dw_shard) % 16)
     return fail(WHALE_ERR_INVALID_ARG, "dx_local / dw_shard must be 16-byte aligned");

@@ -17,14 +17,17 @@ class SplitFCSoftmaxCE:
     """Class-split FC + softmax-CE over ``world`` ranks (shard r <-> rank r).
 
     Args:
-        num_classes: C.  feature_dim: D.  local_batch: B (per rank, equal on all ranks).
-        capacity: optional integer capacity weights (hardware-aware uneven split).
+        num_classes: C.  feature_dim: D.  local_batch: B (per rank; ignored if batch_counts).
+        capacity: optional integer capacity weights (hardware-aware uneven class split).
+        batch_counts: optional per-rank DP batch [world] (hardware-aware ``replicate``, NEXT-3;
+            e.g. ``whale_splitfc_plan(B_tot, world, capacity)``); rank r's rows follow ranks < r.
         dtype: torch.bfloat16 (tcgen05 kind::f16) or torch.float32 (kind::tf32).
         group: torch.distributed process group (None -> world 1).
     """
 
     def __init__(self, num_classes: int, feature_dim: int, local_batch: int, capacity=None,
-                 dtype=torch.bfloat16, group=None, device=None, mem_bytes=None, bytes_per_class=None):
+                 dtype=torch.bfloat16, group=None, device=None, mem_bytes=None, bytes_per_class=None,
+                 batch_counts=None):
         self.C, self.D, self.B = int(num_classes), int(feature_dim), int(local_batch)
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -34,6 +37,13 @@ class SplitFCSoftmaxCE:
         else:
             self.rank, self.world = 0, 1
         self.group = group
+        self.batch_counts = None
+        if batch_counts is not None:
+            self.batch_counts = [int(b) for b in batch_counts]
+            if len(self.batch_counts) != self.world:
+                raise ValueError("batch_counts must have one entry per rank")
+            self.B = self.batch_counts[self.rank]
+        self.row0 = sum(self.batch_counts[:self.rank]) if self.batch_counts else self.rank * self.B
         if mem_bytes is None:
             self.counts, self.offsets = _lib.whale_splitfc_plan(self.C, self.world, capacity)
         else:
@@ -44,7 +54,8 @@ class SplitFCSoftmaxCE:
             self.counts, self.offsets = _lib.whale_splitfc_plan_mem(self.C, self.world, capacity, mem_bytes, bpc)
         self.C_r, self.o_r = self.counts[self.rank], self.offsets[self.rank]
         xdt = {torch.bfloat16: _lib.WHALE_BF16, torch.float32: _lib.WHALE_F32}[dtype]
-        q, _keep = _lib.make_desc(self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt)
+        q, _keep = _lib.make_desc(self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt,
+                                  batch_counts=self.batch_counts)
         symm_bytes, local_bytes = _lib.whale_splitfc_workspace_size(q)
         self.workspace = torch.empty(local_bytes, dtype=torch.uint8, device=self.device)
         peer_ptrs = None
@@ -61,7 +72,7 @@ class SplitFCSoftmaxCE:
             self._symm = (buf, hdl)
         self._desc, self._keep = _lib.make_desc(
             self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt, peer_ptrs, symm_bytes,
-            self.workspace.data_ptr(), local_bytes)
+            self.workspace.data_ptr(), local_bytes, self.batch_counts)
         self.ctx = _lib.whale_splitfc_create(self._desc)
         self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.row_loss = torch.zeros(self.B, dtype=torch.float32, device=self.device)

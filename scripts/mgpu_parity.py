@@ -17,6 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle  # noqa: E402
 import synthetic as syn  # noqa: E402
 from paper_2011_09208_b200 import SplitFCSoftmaxCE  # noqa: E402
+from paper_2011_09208_b200._lib import whale_splitfc_plan as plan  # noqa: E402
 
 
 def fro(a, b):
@@ -25,16 +26,21 @@ def fro(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf16", seed=1, steps=2, bias=False):
-    Bt = B * world
+def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf16", seed=1, steps=2, bias=False,
+             batch=None):
+    bc = batch if batch is not None else [B] * world  # per-rank DP batch (NEXT-3 when uneven)
+    Bt = sum(bc)
+    r0 = sum(bc[:rank])
+    B = bc[rank]
     X = syn.gen_features((0, Bt), D, seed, dtype)
     W = syn.gen_weight((0, C), D, seed, regime, dtype)
     y = syn.gen_labels((0, Bt), C, seed)
     bfull = syn.gen_bias((0, C), seed, 2.0, dtype) if bias else None
-    op = SplitFCSoftmaxCE(C, D, B, capacity=capacity, dtype=syn.torch_dtype(dtype), group=dist.group.WORLD, device=dev)
+    op = SplitFCSoftmaxCE(C, D, B, capacity=capacity, dtype=syn.torch_dtype(dtype), group=dist.group.WORLD, device=dev,
+                          batch_counts=batch)
     o, c = op.o_r, op.C_r
-    xr = X[rank * B:(rank + 1) * B].to(dev)
-    yr = y[rank * B:(rank + 1) * B].to(dev)
+    xr = X[r0:r0 + B].to(dev)
+    yr = y[r0:r0 + B].to(dev)
     wr = W[o:o + c].to(dev).contiguous()
     br = bfull[o:o + c].to(dev).contiguous() if bias else None
     for _ in range(steps):  # repeated steps exercise the device epoch / flag protocol
@@ -48,23 +54,23 @@ def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf1
     dist.all_gather(losses, loss)
     bit_equal = all(torch.equal(l, losses[0]) for l in losses)
     res = {
-        "B": B, "D": D, "C": C, "world": world, "capacity": capacity, "regime": regime, "dtype": dtype,
+        "B": B, "batch": bc, "D": D, "C": C, "world": world, "capacity": capacity, "regime": regime, "dtype": dtype,
         "C_r": c, "loss": float(loss), "loss_ref": float(f["loss"]),
         "loss_rel": abs(float(loss) - f["loss"]) / abs(f["loss"]),
-        "rowloss_rel": fro(op.row_loss.cpu(), f["row_loss"][rank * B:(rank + 1) * B]),
-        "dx_rel": fro(dx.float().cpu(), f["dX"][rank * B:(rank + 1) * B]),
+        "rowloss_rel": fro(op.row_loss.cpu(), f["row_loss"][r0:r0 + B]),
+        "dx_rel": fro(dx.float().cpu(), f["dX"][r0:r0 + B]),
         "dw_rel": fro(dw.cpu(), f["dW"][o:o + c]),
         "loss_bit_equal": bool(bit_equal),
     }
     ok = res["loss_rel"] <= 1e-3 and res["dx_rel"] <= 1e-2 and res["dw_rel"] <= 1e-2 and bit_equal
     if bias:
-        rows = slice(rank * B, (rank + 1) * B)
+        rows = slice(r0, r0 + B)
         Zs = np.sort(f["Z"][rows], axis=1)
         clear = (Zs[:, -1] - Zs[:, -2]) > 1e-3
         pred = op.pred.cpu().numpy()
         res["db_rel"] = fro(out[2].cpu(), f["db"][o:o + c])
         res["pred_ok"] = bool(np.array_equal(pred[clear], f["pred"][rows][clear]))
-        res["prob_rel"] = float(np.max(np.abs(op.prob.cpu().numpy() - f["prob"][rows]) / f["prob"][rows]))
+        res["prob_rel"] = float(np.max(np.abs(op.prob.cpu().numpy() - f["prob"][rows]) / f["prob"][rows])) if B else 0.0
         ok = ok and res["db_rel"] <= 1e-2 and res["pred_ok"] and res["prob_rel"] <= 1e-3
     res["ok"] = ok
     allres = [None] * world
@@ -87,6 +93,11 @@ def main():
         dict(B=64, D=520, C=20000),
         dict(B=32, D=2048, C=100_000),                              # c2 shape
         dict(B=24, D=256, C=7001, regime="peaked", bias=True),      # NEXT-4: bias, db, predictions
+        # NEXT-3: uneven per-rank batch from the proportional plan (2:1:...:1 capacity)
+        dict(B=None, D=512, C=9000, batch=plan(12 * world, world, [2] + [1] * (world - 1))[0]),
+        dict(B=None, D=256, C=7001, regime="peaked", bias=True, batch=plan(10 * world + 3, world, list(range(1, world + 1)))[0]),
+        dict(B=None, D=256, C=3000, batch=[40] * (world - 1) + [0]),  # a rank with no rows
+        dict(B=None, D=2048, C=100_000, batch=plan(32 * world, world, [2] + [1] * (world - 1))[0]),
     ]
     ok = True
     for cs in cases:

@@ -140,3 +140,27 @@ def test_plan_mem_golden_and_matches_oracle():
         assert _lib.whale_splitfc_plan_mem(C, N, w, mem, bpc, fixed) == (list(ref[0]), list(ref[1]))
     # no caps -> identical to the proportional plan
     assert _lib.whale_splitfc_plan_mem(100000, 8, [2] + [1] * 7) == _lib.whale_splitfc_plan(100000, 8, [2] + [1] * 7)
+
+
+def test_batch_counts_descriptor():
+    """NEXT-3: per-rank DP batch.  The proportional batch split is the same
+    largest-remainder plan (worked example: 2:1 capacity on 6 samples -> [4, 2])."""
+    bc, _ = _lib.whale_splitfc_plan(6, 2, [2, 1])
+    assert bc == [4, 2]
+    C, D = 1000, 64
+    counts, offs = _lib.whale_splitfc_plan(C, 2)
+    sizes = {}
+    for rank in (0, 1):
+        d, _k = _lib.make_desc(rank, 2, bc[rank], D, C, counts, offs, batch_counts=bc)
+        sizes[rank] = _lib.whale_splitfc_workspace_size(d)
+    assert sizes[0][0] == sizes[1][0]  # the symmetric buffer is the same size on every rank
+    d_eq, _k = _lib.make_desc(0, 2, 4, D, C, counts, offs)  # equal 4 + 4 needs more than 4 + 2
+    assert _lib.whale_splitfc_workspace_size(d_eq)[0] >= sizes[0][0]
+    # a rank may contribute no rows (it still serves its class shard)
+    d0, _k = _lib.make_desc(1, 2, 0, D, C, counts, offs, batch_counts=[6, 0])
+    _lib.whale_splitfc_workspace_size(d0)
+    for B, bcs in ((3, [4, 2]), (4, [4, -1]), (0, [0, 0])):
+        d, _k = _lib.make_desc(0, 2, B, D, C, counts, offs, batch_counts=bcs)
+        with pytest.raises(_lib.WhaleError) as e:
+            _lib.whale_splitfc_workspace_size(d)
+        assert e.value.status == 1
