@@ -14,6 +14,7 @@
 #include "../../include/whale_splitfc.h"
 #include "gemm_sm100.cuh"
 #include "bwd_sm100.cuh"
+#include "fwd_dx_sm100.cuh"
 #include "kernels_aux.cuh"
 
 using namespace whale;
@@ -183,6 +184,7 @@ struct Layout {
   // local workspace offsets
   size_t P = 0, m_tile = 0, s_tile = 0, zy = 0, lse = 0, row_loss = 0, dxpart = 0, counters = 0, tile_cnt = 0;
   size_t a_tile = 0, dbpart = 0;  // NEXT-4: per-(row, tile) top-1 class; bias-gradient partials
+  size_t upart = 0, uref = 0;     // F1: per-cluster U = sum_t P~_t W_t partials and their row references
   size_t local_total = 0;
   // fp32 (kind::tf32) backward only: K-major transposed operands
   size_t XT = 0, GT = 0, WT = 0;
@@ -203,6 +205,9 @@ struct Plan {
   int64_t Boff[kMaxRanks + 1] = {};  // rank r's rows: [Boff[r], Boff[r+1]) of the gathered batch
   int sms = 148;
   GemmCfg fwd, dw, dx;
+  // F1 (fwd_dx_sm100.cuh): fused logits + dX partials, W_r read once (bf16, B_tot <= 32)
+  bool f1 = false;
+  int f1_ncl = 0, f1_stages = 0, f1_smem = 0, f1_Dq = 0;
   Layout L;
 };
 
@@ -356,6 +361,26 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
     finish_cfg(p.dw, sms, p.dw.num_kb <= 4, p.es, p.es == 2);
   }
   p.dx = choose_splitk(p.Bt, p.D, p.Cr, atom, kbk, sms);
+  {
+    const char* e = getenv("WHALE_F1");
+    p.f1 = p.es == 2 && p.Bt <= kF1NB && p.D % (kF1KC * 128) == 0 && p.D / kF1KC <= 1024 &&
+           !(e && e[0] == '0');
+    if (p.f1) {
+      p.f1_Dq = static_cast<int>(p.D / kF1KC);
+      const int T = cdiv(p.Cr, kF1TileC);
+      p.f1_ncl = std::min(sms / kF1KC, T);  // upper bound; create() lowers it to the co-resident count
+      // stages: provisional here (host-only planning); create() sizes them with the kernel's
+      // real static shared memory
+      const int fixed = f1_smem_bytes(0, p.f1_Dq) + 2048;
+      p.f1_stages = std::min(8, (kSmemLimit - fixed) / kF1StageBytes) & ~1;
+      p.f1_smem = f1_smem_bytes(p.f1_stages, p.f1_Dq);
+      if (p.f1_stages < 4) p.f1 = false;
+    }
+    if (p.f1) {  // the statistics / gradient pipeline sees 128-class tiles
+      p.fwd.BN = kF1TileC;
+      p.fwd.n_blocks = cdiv(p.Cr, kF1TileC);
+    }
+  }
 
   Layout& L = p.L;
   size_t o = 0;
@@ -376,6 +401,10 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   L.tile_cnt = take(static_cast<size_t>(p.dx.m_blocks) * p.dx.n_blocks * 4);
   L.a_tile = take(static_cast<size_t>(p.Bt) * T * 4);
   L.dbpart = take(static_cast<size_t>(cdiv(p.Bt, kDbRows)) * p.Cr * 4);
+  if (p.f1) {
+    L.upart = take(static_cast<size_t>(p.f1_ncl) * p.Bt * p.D * 4);
+    L.uref = take(static_cast<size_t>(p.f1_ncl) * p.Bt * 4);
+  }
   if (p.es == 4) {
     L.ld_bt = static_cast<int64_t>(align_up(p.Bt, 4));
     L.XT = take(static_cast<size_t>(p.D) * L.ld_bt * 4);
@@ -488,7 +517,7 @@ struct whale_splitfc_ctx {
   // pointer-cached maps
   const void* x_cached = nullptr;
   const void* w_cached = nullptr;
-  CUtensorMap tmW_fwd, tmW_dx;
+  CUtensorMap tmW_fwd, tmW_dx, tmW_f1, tmX_f1;
   const void* dw_cached = nullptr;
   CUtensorMap tmDW;
   const void* x_fwd = nullptr;       // N = 1: the forward's X (read again by dW)
@@ -662,6 +691,38 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     if (c->bwd_stages < 2) c->fused_bwd = false;
   }
   if (!c->fused_bwd && p.es == 2) maybe_pair(c->p.dw, sms, true, kRowBytes / p.es);  // standalone dW GEMM
+  if (p.f1) {
+    // F1 clusters must all be co-resident (one wave): not every GPC holds a multiple of KC SMs
+    cudaFuncAttributes fa{};
+    CUDA_TRY(cudaFuncGetAttributes(&fa, splitfc_fwd_dx_kernel));
+    const int fixed = f1_smem_bytes(0, p.f1_Dq) + static_cast<int>(fa.sharedSizeBytes);
+    c->p.f1_stages = std::min(8, (kSmemLimit - fixed) / kF1StageBytes) & ~1;
+    c->p.f1_smem = f1_smem_bytes(c->p.f1_stages, p.f1_Dq);
+    if (c->p.f1_stages < 4) {
+      delete c;
+      return fail(WHALE_ERR_UNSUPPORTED, "F1 shared memory: %d static bytes leave < 4 stages", (int)fa.sharedSizeBytes);
+    }
+    CUDA_TRY(cudaFuncSetAttribute(splitfc_fwd_dx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c->p.f1_ncl * kF1KC);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = p.f1_smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kF1KC;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveClusters(&ncl, splitfc_fwd_dx_kernel, &cfg));
+    if (ncl < 1) {
+      delete c;
+      return fail(WHALE_ERR_UNSUPPORTED, "F1 cluster cannot be resident");
+    }
+    c->p.f1_ncl = std::min(c->p.f1_ncl, ncl);
+  }
   // static TMA maps
   const int es = p.es, kbk = kRowBytes / es, atom = kRowBytes / es;
   if (p.world > 1) {
@@ -669,6 +730,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
       const void* xg = c->symm[p.rank] + p.L.xg;
       MAP_TRY(map2d(&c->tmX_fwd, xg, es, p.D, p.Bt, p.D * es, kbk, kBM));
       MAP_TRY(map2d(&c->tmX_dw, xg, es, p.D, p.Bt, p.D * es, atom, p.dw.bk));
+      if (p.f1) MAP_TRY(map2d(&c->tmX_f1, xg, es, p.D, p.Bt, p.D * es, 64, kF1NB));
     }
   }
   void* P = c->ws + p.L.P;
@@ -710,6 +772,10 @@ static whale_status_t ensure_w_maps(whale_splitfc_ctx* c, const void* w) {
   if (st != WHALE_OK) return st;
   st = map2d(&c->tmW_dx, w, p.es, p.D, p.Cr, p.D * p.es, atom, kbk);
   if (st != WHALE_OK) return st;
+  if (p.f1) {
+    st = map2d(&c->tmW_f1, w, p.es, p.D, p.Cr, p.D * p.es, 64, kF1TileC);
+    if (st != WHALE_OK) return st;
+  }
   c->w_cached = w;
   return WHALE_OK;
 }
@@ -724,6 +790,10 @@ static whale_status_t ensure_x_maps(whale_splitfc_ctx* c, const void* x) {
   if (st != WHALE_OK) return st;
   st = map2d(&c->tmX_dw, x, p.es, p.D, p.Bt, p.D * p.es, atom, p.dw.bk);
   if (st != WHALE_OK) return st;
+  if (p.f1) {
+    st = map2d(&c->tmX_f1, x, p.es, p.D, p.Bt, p.D * p.es, 64, kF1NB);
+    if (st != WHALE_OK) return st;
+  }
   c->x_cached = x;
   return WHALE_OK;
 }
@@ -775,7 +845,53 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
                      env_int("WHALE_GATHER_DBG", 0))));
   }
   // ---- A3 logits GEMM with fused row statistics
-  {
+  if (ES == 2 && p.f1) {
+    // F1: logits + statistics + dX partials U in one pass over W_r (fwd_dx_sm100.cuh)
+    F1Args a{};
+    a.Bt = static_cast<int>(p.Bt);
+    a.D = static_cast<int>(p.D);
+    a.Dq = p.f1_Dq;
+    a.C_r = static_cast<int>(p.Cr);
+    a.num_tiles = p.fwd.n_blocks;
+    a.stages = p.f1_stages;
+    a.class_offset = p.o_r;
+    a.labels = yg;
+    a.bias = bias;
+    a.m_tile = wsp<float>(c, L.m_tile);
+    a.s_tile = wsp<float>(c, L.s_tile);
+    a.zy = wsp<float>(c, L.zy);
+    a.a_tile = wsp<int32_t>(c, L.a_tile);
+    a.P = wsp<__nv_bfloat16>(c, L.P);
+    a.ldp = p.ldp;
+    a.upart = wsp<float>(c, L.upart);
+    a.uref = wsp<float>(c, L.uref);
+    a.dev_epoch = dev_epoch;
+    a.err = err;
+    a.debug = env_int("WHALE_F1_DBG", 0);
+    if (p.world > 1) {
+      a.wait_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_GATHER * kMaxRanks;
+      a.wait_count = p.world;
+      a.wait_mult = static_cast<uint32_t>(gather_grid(p));
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.f1_ncl * kF1KC);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = p.f1_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kF1KC;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = c->pdl ? 2 : 1;
+    PROFILED(K_LOGITS, s, ([&]() -> whale_status_t {
+               CUDA_TRY(cudaLaunchKernelEx(&cfg, splitfc_fwd_dx_kernel, c->tmW_f1, c->tmX_f1, a));
+               return WHALE_OK;
+             }()));
+  } else {
     GemmArgs a = base_args(p.fwd, static_cast<int>(p.Bt), static_cast<int>(p.Cr));
     a.dev_epoch = dev_epoch;
     a.labels = yg;
@@ -832,6 +948,9 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.pred_local = pred;
     a.prob_local = prob;
     a.grad_vecs = static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(4, (p.fwd.n_blocks * 10 + 511) / 512)));
+    // F1 (B_tot <= 32, 128-class tiles): the per-CTA partial re-read comes from L2 and the
+    // grid is short (B_tot rows) -> small chunks for enough loads in flight
+    if (p.f1) a.grad_vecs = env_int("WHALE_F1_GV", 4);
     const int64_t chunk = static_cast<int64_t>(kStatsThreads) * a.grad_vecs * (16 / ES);
     if (p.world == 1) {
       // A4-A6 fused: lse, loss and G in one pass (no exchange needed)
@@ -953,8 +1072,25 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       ax.rs_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_RS * kMaxRanks + p.rank;
     }
   }
+  if (ES == 2 && p.f1) {
+    // ---- A8 from the forward's U partials: dX = (1/B_tot)(sum_cl e^{ref - lse} U_cl - W_y)
+    RowSplit rs{};
+    PeerPtrs recv{};
+    for (int r = 0; r <= p.world; ++r) rs.off[r] = static_cast<int>(p.Boff[r]);
+    if (p.world > 1)
+      for (int r = 0; r < p.world; ++r) recv.p[r] = c->symm[r] + L.dxrecv;
+    PROFILED(K_DX, s,
+             (launch(c, dx_combine_kernel<2>, dim3(cdiv(p.D / 4, 32), static_cast<unsigned>(p.Bt)), dim3(256), 0,
+                     s, static_cast<const float*>(wsp<float>(c, L.upart)),
+                     static_cast<const float*>(wsp<float>(c, L.uref)), p.f1_ncl, static_cast<int>(p.Bt),
+                     static_cast<int>(p.D), static_cast<const float*>(wsp<float>(c, L.lse)), yg,
+                     static_cast<long long>(p.o_r), static_cast<long long>(p.Cr), w,
+                     static_cast<float>(1.0 / static_cast<double>(p.Bt)), dx_local, recv, rs, p.rank, p.world,
+                     static_cast<int>(p.Bmax))));
+  }
   if (ES == 2 && c->fused_bwd) {
     // ---- A7 + A8 in one persistent launch: dX units first (one per CTA), then dW tiles
+    //      (F1: dX came from the forward -> dW tiles only)
     BwdArgs b{};
     b.dx = ax;
     b.dw = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
@@ -963,7 +1099,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     // once) across all D-column blocks; M-fastest re-read G once per column block (c5: 16x)
     b.dw.n_fastest = g_dw_m_fastest ? 0 : 1;
     b.dw.err = err;
-    b.ux = p.dx.num_tiles;
+    b.ux = p.f1 ? 0 : p.dx.num_tiles;
     b.tw = p.dw.num_tiles;
     b.stages = c->bwd_stages;
     b.stage_bytes = c->bwd_stage_bytes;
@@ -1129,7 +1265,8 @@ extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, cha
   std::string s = std::string(head) + "\"fwd\":" + g(p.fwd) + ",\"dw\":" + g(p.dw) + ",\"dx\":" + g(p.dx) +
                   ",\"off_P\":" + std::to_string(p.L.P) + ",\"off_m_tile\":" + std::to_string(p.L.m_tile) +
                   ",\"off_s_tile\":" + std::to_string(p.L.s_tile) + ",\"off_lse\":" + std::to_string(p.L.lse) +
-                  ",\"off_dxpart\":" + std::to_string(p.L.dxpart) +
+                  ",\"off_dxpart\":" + std::to_string(p.L.dxpart) + ",\"f1\":" + std::to_string(p.f1 ? 1 : 0) +
+                  ",\"f1_clusters\":" + std::to_string(p.f1_ncl) + ",\"f1_stages\":" + std::to_string(p.f1_stages) +
                   ",\"local_bytes\":" + std::to_string(p.L.local_total) +
                   ",\"symm_bytes\":" + std::to_string(p.L.symm_total) + "}";
   if (s.size() + 1 > buf_len) return fail(WHALE_ERR_INVALID_ARG, "buffer too small (%zu)", s.size() + 1);
@@ -1162,4 +1299,34 @@ extern "C" int whale_debug_trace_read(unsigned long long* out) {
   if (cudaDeviceSynchronize() != cudaSuccess) return -1;
   if (cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 32) != cudaSuccess) return -1;
   return whale_debug_trace_enable(1);
+}
+
+// Internal (not in the public header): how many KC-CTA clusters of the F1 kernel with
+// `smem` dynamic bytes can be co-resident on this device (cudaOccupancyMaxActiveClusters).
+extern "C" int whale_debug_f1_max_clusters(int smem) {
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, splitfc_fwd_dx_kernel) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(splitfc_fwd_dx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kSmemLimit - static_cast<int>(fa.sharedSizeBytes)) != cudaSuccess)
+    return -2;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(148);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kF1KC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, splitfc_fwd_dx_kernel, &cfg) != cudaSuccess) return -3;
+  return n;
+}
+
+// Internal: read the F1 debug timeline (64 periods x 8 stamps, ns).  Synchronises the device.
+extern "C" int whale_debug_f1_timeline(unsigned long long* out) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  return cudaMemcpyFromSymbol(out, g_f1_ts, sizeof(g_f1_ts)) == cudaSuccess ? 0 : -2;
 }

@@ -87,6 +87,30 @@ def test_parity_small_bf16(whale, B, D, C, regime):
     _check_full(g, f, f"{B}x{D}x{C}/{regime}")
 
 
+# Shapes that take the fused forward + dX path (F1: bf16, B_tot <= 32, D % 512 == 0, D <= 2048):
+# single class tile, ragged last tile, several tiles per cluster, more clusters than tiles.
+F1_SHAPES = [
+    (32, 512, 100),                # one ragged tile, 36 idle clusters
+    (1, 512, 129),                 # single row, 2 tiles (second holds one class)
+    (17, 1024, 3001),              # ragged rows, ragged last tile
+    (32, 2048, 20_000),            # 157 tiles over 37 clusters
+    (24, 1536, 9000),              # D quarter of 384 (3 G2 blocks)
+]
+
+
+@pytest.mark.parametrize("B,D,C", F1_SHAPES)
+@pytest.mark.parametrize("regime", ["init", "peaked"])
+def test_parity_f1(whale, B, D, C, regime):
+    seed = 300 + B + D + C
+    X = syn.gen_features((0, B), D, seed, "bf16")
+    W = syn.gen_weight((0, C), D, seed, regime, "bf16")
+    y = syn.gen_labels((0, B), C, seed)
+    g = _run(whale, X, W, y)
+    assert g["cfg"]["f1"] == 1
+    f = oracle.forward_backward(X, W, y.numpy())
+    _check_full(g, f, f"f1 {B}x{D}x{C}/{regime}")
+
+
 def test_parity_tiny_fp32(whale):
     """configs[0] tiny: B=8 per rank x 2 ranks = 16 rows, D=64, C=1000, fp32 operands
     (kind::tf32, DESIGN.md R11), single-GPU view of the whole global batch."""
