@@ -98,6 +98,9 @@ def main():
         dict(B=None, D=256, C=7001, regime="peaked", bias=True, batch=plan(10 * world + 3, world, list(range(1, world + 1)))[0]),
         dict(B=None, D=256, C=3000, batch=[40] * (world - 1) + [0]),  # a rank with no rows
         dict(B=None, D=2048, C=100_000, batch=plan(32 * world, world, [2] + [1] * (world - 1))[0]),
+        # F1 path (fused forward + dX; B_tot <= 32, D % 256 == 0): total batch 32
+        dict(B=32 // world, D=2048, C=100_000),
+        dict(B=None, D=1024, C=30_011, regime="peaked", bias=True, batch=plan(32, world, list(range(1, world + 1)))[0]),
     ]
     ok = True
     for cs in cases:
