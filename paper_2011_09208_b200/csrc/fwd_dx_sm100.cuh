@@ -21,14 +21,18 @@
 // from L2, so DRAM sees W once.  (KC = 2, not 4: every CTA of a cluster repeats the tile's
 // softmax epilogue, so fewer, larger D parts halve that work; TMEM holds U for D/2 <= 1024.)
 //
-// The per-(row, tile) statistics written for the rest of the pipeline are the same as the
-// logits GEMM's EPI_FWD_STATS epilogue: m_tile = tile max, s_tile = sum exp(z - m_tile),
-// P~ = exp(z - m_tile) in bf16 (the backward's dW operand), z_y, a_tile (top-1 class).
+// The per-(row, tile) statistics written for the rest of the pipeline generalise the
+// logits GEMM's EPI_FWD_STATS epilogue: m_tile = the row's reference for the tile,
+// s_tile = sum exp(z - m_tile), P~ = exp(z - m_tile) in bf16 (the backward's dW operand,
+// TMA-stored straight from the G2 operand buffer), z_y, plus mx_tile = the true tile max and
+// a_tile = its class (predictions).  Any reference gives the same lse; the statistics
+// kernels take the row max from mx_tile.
 //
 //   warp 0      TMA producer (one lane): X part once (resident), then W chunks in MMA order
 //   warp 1      MMA issuer (one lane):   period p = G1(p) interleaved with G2(p - 2)
 //   warp 2      TMEM allocator (512 columns: Z x 2 and U blocks x D_q/128, 32 columns each)
-//   warps 4..7  epilogue: thread = class row of the tile (TMEM lane)
+//   warp 3      TMA producer for the G2 ring (L2 re-reads)
+//   warps 4..11 epilogue: thread = class row of the tile (TMEM lane) x 16 batch columns
 #pragma once
 #include "gemm_sm100.cuh"
 
@@ -42,6 +46,11 @@ constexpr int kF1XChunkBytes = kF1NB * kRowBytes;    // 32 rows x 64 D bf16 = 4 
 constexpr int kF1SlotBytes = kF1TileC * kF1NB * 4;   // one partial Z_t^T, fp32 = 16 KB
 constexpr int kF1PBytes = 2 * kF1NB * kRowBytes;     // P~_t^T operand: 2 atoms x 32 rows x 128 B
 constexpr int kF1TmemCols = 512;
+constexpr int kF1G1SlotBytes = kF1StageBytes + kF1XChunkBytes;  // G1 ring slot: W chunk + X chunk
+constexpr int kF1G2SlotBytes = 2 * kF1StageBytes;                 // G2 ring slot: 128 D rows of W
+constexpr int kF1S2 = 2;                                          // G2 ring slots
+constexpr int kF1EpiThreads = 256;                                // 8 epilogue warps
+constexpr int kF1Threads = 128 + kF1EpiThreads;
 constexpr float kF1Tau = 8.0f;  // lazy rescale threshold, log2 units
 
 struct F1Args {
@@ -49,16 +58,15 @@ struct F1Args {
   int D, Dq;               // feature dim, D / KC (multiple of 128, <= 1024)
   int C_r;                 // classes of this shard
   int num_tiles;           // ceil(C_r / 128) = T
-  int stages;              // W ring stages (even)
+  int stages;              // G1 ring slots
   long long class_offset;  // o_r
   const int32_t* labels;   // [Bt] global class ids
   const void* bias;        // [C_r] bf16 or NULL
-  float* m_tile;           // [Bt x T]
+  float* m_tile;           // [Bt x T] reference the tile's P~ and s_tile are relative to
   float* s_tile;           // [Bt x T]
+  float* mx_tile;          // [Bt x T] true tile max
   float* zy;               // [Bt]
   int32_t* a_tile;         // [Bt x T] global class id of the tile's max, or NULL
-  __nv_bfloat16* P;        // P~ [Bt x ldp]
-  long long ldp;
   float* upart;            // [ncl x Bt x D] per-cluster U (relative to uref)
   float* uref;             // [ncl x Bt]
   const uint32_t* wait_flags;  // N > 1: gather flags (as GemmArgs)
@@ -70,11 +78,13 @@ struct F1Args {
                            // bit 1 = skip G2 (dX wrong)
 };
 
-// Debug timeline (CTA 0): [period][8] globaltimer stamps, see splitfc_fwd_dx_kernel.
-__device__ unsigned long long g_f1_ts[64 * 8];
+// Debug timeline (CTA 0): [period][16] globaltimer stamps, see splitfc_fwd_dx_kernel.
+__device__ unsigned long long g_f1_ts[64 * 16];
+__device__ unsigned long long g_f1_cta[160 * 3];  // per-CTA [entry, after prologue, end] (debug bit 0)
 
 __host__ __device__ constexpr int f1_smem_bytes(int stages, int Dq) {
-  return 1024 + stages * kF1StageBytes + (Dq / 64) * kF1XChunkBytes + (kF1KC - 1) * kF1SlotBytes + 2 * kF1PBytes + 240;
+  return 1024 + stages * kF1G1SlotBytes + kF1S2 * kF1G2SlotBytes + (kF1KC - 1) * kF1SlotBytes + 2 * kF1PBytes + 256 +
+         0 * Dq;
 }
 
 // Warp-wide fp32 max (sm_100a redux.sync .f32), result in every lane.
@@ -99,29 +109,33 @@ __device__ __forceinline__ void f1_colsum32(float (&v)[32], int lane) {
   }
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kF1Threads, 1)
     splitfc_fwd_dx_kernel(const __grid_constant__ CUtensorMap tmW /*box {64, 128}*/,
-                          const __grid_constant__ CUtensorMap tmX /*box {64, 32}*/, const F1Args a) {
+                          const __grid_constant__ CUtensorMap tmX /*box {64, 32}*/,
+                          const __grid_constant__ CUtensorMap tmP /*P~ [B_tot x C_r], box {64, 32}*/, const F1Args a) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ float red_v[4][32];
   __shared__ int red_i[4][32];
-  __shared__ float s_ref[32], s_c[32], s_fac[32], s_max[32];
+  __shared__ __align__(16) float s_ref[32];
+  __shared__ float s_fac[32], s_max[32];
   __shared__ int s_arg[32], s_lab[32];
   __shared__ int s_rescale;
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int KQ = a.Dq / 64;  // 64-wide D chunks of this CTA's part
-  uint8_t* ring = smem;
-  uint8_t* xres = ring + a.stages * kF1StageBytes;
-  uint8_t* recv = xres + KQ * kF1XChunkBytes;
+  const int S1 = a.stages;   // G1 ring: W chunk (16 KB) + X chunk (4 KB) per slot
+  uint8_t* ring1 = smem;
+  uint8_t* ring2 = ring1 + S1 * kF1G1SlotBytes;  // G2 ring: one 128-D block (2 W chunks) per slot
+  uint8_t* recv = ring2 + kF1S2 * kF1G2SlotBytes;
   uint8_t* pbuf = recv + (kF1KC - 1) * kF1SlotBytes;  // 2 buffers
-  uint64_t* full = reinterpret_cast<uint64_t*>(pbuf + 2 * kF1PBytes);
-  uint64_t* empty = full + a.stages;
-  uint64_t* zfull = empty + a.stages;  // 3 Z buffers
+  uint64_t* full1 = reinterpret_cast<uint64_t*>(pbuf + 2 * kF1PBytes);
+  uint64_t* empty1 = full1 + S1;
+  uint64_t* full2 = empty1 + S1;
+  uint64_t* empty2 = full2 + kF1S2;
+  uint64_t* zfull = empty2 + kF1S2;  // 3 Z buffers
   uint64_t* zempty = zfull + 3;
-  uint64_t* pfull = zempty + 3;        // 2 P~ buffers
-  uint64_t* pempty = pfull + 2;        // completes when G2 of that buffer's tile finished
-  uint64_t* xbar = pempty + 2;
-  uint64_t* xfull = xbar + 1;
+  uint64_t* pfull = zempty + 3;      // 2 P~ buffers
+  uint64_t* pempty = pfull + 2;      // completes when G2 of that buffer's tile finished
+  uint64_t* xfull = pempty + 2;
   uint64_t* xempty = xfull + 1;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xempty + 1);
 
@@ -132,21 +146,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int ncl = static_cast<int>(ncluster_x());
   const int my_tiles = cl < a.num_tiles ? (a.num_tiles - 1 - cl) / ncl + 1 : 0;
   const uint32_t ucol0 = 3 * kF1NB;  // TMEM: Z buffers at 0, 32, 64; U blocks from 96
+  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) g_f1_cta[blockIdx.x * 3] = gtime_ns();
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < a.stages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < S1; ++i) {
+      mbar_init(&full1[i], 1);
+      mbar_init(&empty1[i], 1);
+    }
+    for (int i = 0; i < kF1S2; ++i) {
+      mbar_init(&full2[i], 1);
+      mbar_init(&empty2[i], 1);
     }
     for (int i = 0; i < 3; ++i) {
       mbar_init(&zfull[i], 1);
-      mbar_init(&zempty[i], 128);
+      mbar_init(&zempty[i], kF1EpiThreads);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&pfull[i], 128);
+      mbar_init(&pfull[i], kF1EpiThreads);
       mbar_init(&pempty[i], 1);
     }
-    mbar_init(xbar, 1);
     mbar_init(xfull, 1);
     mbar_init(xempty, kF1KC - 1);
     fence_mbar_init();
@@ -154,6 +172,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (threadIdx.x == 32) {
     tma_prefetch_desc(&tmW);
     tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmP);
   }
   if (warp == 2) tmem_alloc(tmem_holder, kF1TmemCols);
   tc_fence_before();
@@ -166,46 +185,55 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   TraceScope _trace(1);
   const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;
   const int d0 = static_cast<int>(q) * a.Dq;  // first feature column of this CTA's part
+  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) g_f1_cta[blockIdx.x * 3 + 1] = gtime_ns();
 
-  // Schedule (producer and MMA walk the same sequence): period p streams G1 of tile p from
-  // HBM interleaved with G2 of tile p - 2 from L2, in units of [G1 chunk pair, G2 block]
-  // (a G2 block = the two chunks of 128 D rows).  The lag of two periods gives every tile's
-  // epilogue a whole period before its P~ is needed, so neither stream waits on it.
-  if (warp == 0) {
-    // ===================== TMA producer =====================
+  // Schedule: G1 of tile p streams through ring 1 (from HBM); G2 of tile p - 1 re-reads its
+  // W part through ring 2 (from L2, one period after G1 brought it in); the MMA issuer
+  // interleaves G2 blocks between G1 chunk pairs as soon as tile p - 1's epilogue has
+  // published P~.  Separate rings let the HBM stream keep all of ring 1 in flight while the
+  // short-latency L2 re-reads cycle through the small ring 2.
+  if (warp == 0 || warp == 3) {
+    // ===================== TMA producers: warp 0 -> ring 1 (G1), warp 3 -> ring 2 (G2) =====
     if (lane == 0) {
       if (a.wait_flags != nullptr) {
         for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, 8);
         fence_proxy_async_global();
       }
-      mbar_arrive_expect_tx(xbar, static_cast<uint32_t>(KQ * kF1XChunkBytes));
-      for (int k = 0; k < KQ; ++k) tma_load_2d(xres + k * kF1XChunkBytes, &tmX, xbar, d0 + k * 64, 0);
-      int stage = 0;
-      uint32_t phase = 0;
       // L2 policy: G1 reads keep their lines (evict_last) until G2 re-reads them two periods
       // later (evict_first: last use), so DRAM sees W_r once
       const uint64_t keep = l2_policy_evict_last(), drop = l2_policy_evict_first();
-      auto load_w = [&](int it, int k, uint64_t pol) {
-        mbar_wait(&empty[stage], phase ^ 1u);
-        mbar_arrive_expect_tx(&full[stage], kF1StageBytes);
-        tma_load_2d_hint(ring + stage * kF1StageBytes, &tmW, &full[stage], d0 + k * 64, (cl + it * ncl) * kF1TileC,
-                         pol);
-        if (++stage == a.stages) {
-          stage = 0;
-          phase ^= 1u;
-        }
-      };
-      const bool dbg = (a.debug & 1) && blockIdx.x == 0;
-      for (int p = 0; p < my_tiles + 2; ++p) {
-        if (dbg && p < 64) g_f1_ts[p * 8 + 7] = gtime_ns();
-        for (int i = 0; i < KQ / 2; ++i) {
-          if (p < my_tiles) {
-            load_w(p, 2 * i, keep);
-            load_w(p, 2 * i + 1, keep);
+      const bool dbg = (a.debug & 1) && blockIdx.x == 0 && warp == 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      if (warp == 0) {
+        for (int it = 0; it < my_tiles; ++it) {
+          if (dbg && it < 64) g_f1_ts[it * 16 + 7] = gtime_ns();
+          const int row0 = (cl + it * ncl) * kF1TileC;
+          for (int k = 0; k < KQ; ++k) {
+            mbar_wait(&empty1[stage], phase ^ 1u);
+            uint8_t* slot = ring1 + stage * kF1G1SlotBytes;
+            mbar_arrive_expect_tx(&full1[stage], kF1StageBytes + kF1XChunkBytes);
+            tma_load_2d_hint(slot, &tmW, &full1[stage], d0 + k * 64, row0, keep);
+            tma_load_2d(slot + kF1StageBytes, &tmX, &full1[stage], d0 + k * 64, 0);
+            if (++stage == S1) {
+              stage = 0;
+              phase ^= 1u;
+            }
           }
-          if (p >= 2 && !(a.debug & 2)) {  // debug bit 2: timing experiment without G2
-            load_w(p - 2, 2 * i, drop);
-            load_w(p - 2, 2 * i + 1, drop);
+        }
+      } else if (!(a.debug & 2)) {  // debug bit 2: timing experiment without G2
+        for (int it = 0; it < my_tiles; ++it) {
+          const int row0 = (cl + it * ncl) * kF1TileC;
+          for (int m = 0; m < KQ / 2; ++m) {
+            mbar_wait(&empty2[stage], phase ^ 1u);
+            uint8_t* slot = ring2 + stage * kF1G2SlotBytes;
+            mbar_arrive_expect_tx(&full2[stage], 2 * kF1StageBytes);
+            tma_load_2d_hint(slot, &tmW, &full2[stage], d0 + (2 * m) * 64, row0, drop);
+            tma_load_2d_hint(slot + kF1StageBytes, &tmW, &full2[stage], d0 + (2 * m + 1) * 64, row0, drop);
+            if (++stage == kF1S2) {
+              stage = 0;
+              phase ^= 1u;
+            }
           }
         }
       }
@@ -215,94 +243,109 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       const uint32_t idesc1 = umma_idesc(kF1TileC, kF1NB, false, false, 1u);
       const uint32_t idesc2 = umma_idesc(128, kF1NB, true, false, 1u);
-      mbar_wait(xbar, 0);
-      tc_fence_after();
-      int stage = 0;
-      uint32_t phase = 0;
-      const uint32_t ring_s = smem_u32(ring), x_s = smem_u32(xres), p_s = smem_u32(pbuf);
+      int s1 = 0, s2 = 0;
+      uint32_t ph1 = 0, ph2 = 0;
+      const uint32_t r1 = smem_u32(ring1), r2 = smem_u32(ring2), p_s = smem_u32(pbuf);
       const bool dbg = (a.debug & 1) && blockIdx.x == 0;
-      for (int p = 0; p < my_tiles + 2; ++p) {
-        const bool has1 = p < my_tiles, has2 = p >= 2;
-        if (dbg && p < 64) g_f1_ts[p * 8 + 0] = gtime_ns();
+      auto g2_block = [&](int j, int i) {  // one G2 block: U^T[128 D rows of block i] += W^T P~_j^T
+        mbar_wait(&full2[s2], ph2);
+        tc_fence_after();
+        const uint32_t aS = r2 + s2 * kF1G2SlotBytes;
+        const uint32_t bS = p_s + (j & 1) * kF1PBytes;
+#pragma unroll
+        for (int kk = 0; kk < kF1TileC / 16; ++kk) {
+          const uint64_t ad = umma_sdesc(aS + kk * 2048, kF1StageBytes, 1024);  // MN-major: 16 class rows / step
+          const uint64_t bd = umma_sdesc(bS + (kk >> 2) * (kF1NB * kRowBytes) + (kk & 3) * 32, 16, 1024);
+          umma_bf16(tmem_base + ucol0 + i * kF1NB, ad, bd, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&empty2[s2]);
+        if (++s2 == kF1S2) {
+          s2 = 0;
+          ph2 ^= 1u;
+        }
+      };
+      // Period p: G1 of tile p, with G2 of tile p - 1 interleaved (one block per G1 chunk pair)
+      // as soon as that tile's epilogue has published P~, and drained at the period end -- so
+      // G2 re-reads W about one period after G1 brought it into L2 (short reuse distance).
+      // G2 order, and hence U's summation order, is fixed.
+      for (int p = 0; p <= my_tiles; ++p) {
+        const bool has1 = p < my_tiles, has2 = p >= 1 && !(a.debug & 2);
+        if (dbg && p < 64) g_f1_ts[p * 16 + 0] = gtime_ns();
         const int zb = p % 3;
-        const int j = p - 2;  // G2 tile
+        const int j = p - 1;  // G2 tile
         if (has1) {
           mbar_wait(&zempty[zb], ((p / 3) & 1) ^ 1u);
           tc_fence_after();
         }
-        if (has2) {
-          mbar_wait(&pfull[j & 1], (j >> 1) & 1);  // P~_j^T in smem (and U rescaled if needed)
-          tc_fence_after();
-        }
-        for (int i = 0; i < KQ / 2; ++i) {
-          if (has1) {
-            for (int h = 0; h < 2; ++h) {
-              const int k = 2 * i + h;
-              mbar_wait(&full[stage], phase);
-              tc_fence_after();
-              const uint32_t aS = ring_s + stage * kF1StageBytes;
-              const uint32_t bS = x_s + k * kF1XChunkBytes;
-              if (a.debug & 8) {  // timing experiment: consume the stage without MMAs
-                mbar_arrive(&empty[stage]);
-              } else {
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  umma_bf16(tmem_base + zb * kF1NB, umma_sdesc(aS + kk * 32, 16, 1024),
-                            umma_sdesc(bS + kk * 32, 16, 1024), idesc1, (k > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(&empty[stage]);
-              }
-              if (++stage == a.stages) {
-                stage = 0;
-                phase ^= 1u;
-              }
-            }
-            if (i == KQ / 2 - 1) {
-              if (a.debug & 8) mbar_arrive(&zfull[zb]);
-              else umma_commit(&zfull[zb]);
-              if (dbg && p < 64) g_f1_ts[p * 8 + 1] = gtime_ns();
-            }
-          }
-          if (has2 && !(a.debug & 2)) {
-            const int s0 = stage;  // even (ring size and every unit are even)
-            mbar_wait(&full[s0], phase);
-            mbar_wait(&full[s0 + 1], phase);
+        int g2_next = 0;
+        bool g2_ready = false;
+        const uint32_t pf = smem_u32(&pfull[(j + 2) & 1]);
+        const uint32_t pf_par = static_cast<uint32_t>((j >> 1) & 1);
+        for (int i = 0; i < KQ / 2 && has1; ++i) {
+          for (int h = 0; h < 2; ++h) {
+            const int k = 2 * i + h;
+            mbar_wait(&full1[s1], ph1);
             tc_fence_after();
-            const uint32_t aS = ring_s + s0 * kF1StageBytes;
-            const uint32_t bS = p_s + (j & 1) * kF1PBytes;
+            const uint32_t aS = r1 + s1 * kF1G1SlotBytes;
+            const uint32_t bS = aS + kF1StageBytes;
+            if (a.debug & 8) {  // timing experiment: consume the slot without MMAs
+              mbar_arrive(&empty1[s1]);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < kF1TileC / 16; ++kk) {
-              const uint64_t ad = umma_sdesc(aS + kk * 2048, kF1StageBytes, 1024);  // MN-major: 16 class rows / step
-              const uint64_t bd = umma_sdesc(bS + (kk >> 2) * (kF1NB * kRowBytes) + (kk & 3) * 32, 16, 1024);
-              umma_bf16(tmem_base + ucol0 + i * kF1NB, ad, bd, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16(tmem_base + zb * kF1NB, umma_sdesc(aS + kk * 32, 16, 1024),
+                          umma_sdesc(bS + kk * 32, 16, 1024), idesc1, (k > 0 || kk > 0) ? 1u : 0u);
+              umma_commit(&empty1[s1]);
             }
-            umma_commit(&empty[s0]);
-            umma_commit(&empty[s0 + 1]);
-            stage += 2;
-            if (stage == a.stages) {
-              stage = 0;
-              phase ^= 1u;
+            if (++s1 == S1) {
+              s1 = 0;
+              ph1 ^= 1u;
             }
+          }
+          if (i == KQ / 2 - 1) {
+            if (a.debug & 8) mbar_arrive(&zfull[zb]);
+            else umma_commit(&zfull[zb]);
+            if (dbg && p < 64) g_f1_ts[p * 16 + 1] = gtime_ns();
+          }
+          if (has2 && g2_next < KQ / 2) {
+            if (!g2_ready && mbar_test(pf, pf_par)) {
+              g2_ready = true;
+              tc_fence_after();
+            }
+            if (g2_ready) g2_block(j, g2_next++);
           }
         }
         if (has2) {
+          if (!g2_ready) {
+            mbar_wait(&pfull[j & 1], pf_par);  // P~_j^T in smem (and U rescaled if needed)
+            tc_fence_after();
+          }
+          while (g2_next < KQ / 2) g2_block(j, g2_next++);
           if (a.debug & 8) mbar_arrive(&pempty[j & 1]);
           else umma_commit(&pempty[j & 1]);
+        } else if (p >= 1) {  // debug bit 2: G2 skipped, keep the P~ buffer protocol alive
+          mbar_wait(&pfull[j & 1], pf_par);
+          mbar_arrive(&pempty[j & 1]);
         }
-        if (dbg && p < 64) g_f1_ts[p * 8 + 2] = gtime_ns();
+        if (dbg && p < 64) g_f1_ts[p * 16 + 2] = gtime_ns();
       }
     }
   } else if (warp >= 4) {
-    // ===================== epilogue: thread = class row of the tile =====================
-    const int et = threadIdx.x - 128;
-    const int qd = warp & 3;
+    // ===================== epilogue: 8 warps, thread = (class row, 16 batch columns) ========
+    // warp 4 + e: TMEM lane quadrant e % 4 (class rows), batch columns [16 (e / 4), + 16)
+    const int et = threadIdx.x - 128;  // 0 .. 255
+    const int ew = warp - 4;
+    const int qd = ew & 3;
+    const int c0 = (ew >> 2) * 16;      // first batch column of this thread
     const int cl_row = qd * 32 + lane;  // class within the tile = TMEM lane
     const bool store_role = (qd % kF1KC) == static_cast<int>(q);  // one CTA stores each class row
     constexpr float kL2e = 1.4426950408889634f;
+    constexpr int kE = kF1EpiThreads;
     if (et < 32) {
       s_lab[et] = et < a.Bt ? a.labels[et] : -1;
       s_ref[et] = -INFINITY;
     }
-    named_bar_sync(2, 128);
+    named_bar_sync(2, kE);
     const uint32_t lane_off = static_cast<uint32_t>(qd * 32) << 16;
     const uint32_t xfull_s = smem_u32(xfull), xempty_s = smem_u32(xempty);
     const uint32_t my_slot_row = smem_u32(recv) + cl_row * 128;
@@ -320,14 +363,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         continue;
       }
       mbar_wait(&zfull[zb], (it / 3) & 1);
-      if (dbg) g_f1_ts[it * 8 + 3] = gtime_ns();
+      if (dbg) g_f1_ts[it * 16 + 3] = gtime_ns();
       tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(tmem_base + zb * kF1NB + lane_off, v);
+      uint32_t v[16];
+      tmem_ld16(tmem_base + zb * kF1NB + c0 + lane_off, v);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&zempty[zb]);
-    // ---- all-reduce of the partial Z_t^T over the cluster (DSMEM), fixed rank order
+      // ---- all-reduce of the partial Z_t^T over the cluster (DSMEM), fixed rank order
       if (it > 0) mbar_wait(xempty, (it - 1) & 1);  // peers consumed my previous partial
 #pragma unroll
       for (uint32_t p = 0; p < kF1KC; ++p) {
@@ -336,53 +379,63 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t dst = mapa_smem(my_slot_row + slot * kF1SlotBytes, p);
         const uint32_t bar = mapa_smem(xfull_s, p);
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch)
-          st_async_v4(dst + ((ch ^ (cl_row & 7)) << 4), bar, v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+        for (int c = 0; c < 4; ++c) {
+          const int ch = (c0 >> 2) + c;
+          st_async_v4(dst + ((ch ^ (cl_row & 7)) << 4), bar, v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        }
       }
       if (et == 0) mbar_arrive_expect_tx(xfull, (kF1KC - 1) * kF1SlotBytes);
       mbar_wait(xfull, it & 1);  // st.async data is visible once its complete_tx lands
-      if (dbg) g_f1_ts[it * 8 + 4] = gtime_ns();
-      float z[32];
+      if (dbg) g_f1_ts[it * 16 + 4] = gtime_ns();
+      float z[16];
 #pragma unroll
       for (uint32_t src = 0; src < kF1KC; ++src) {
-        float pv[32];
+        float pv[16];
         if (src == q) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) pv[j] = __uint_as_float(v[j]);
+          for (int j = 0; j < 16; ++j) pv[j] = __uint_as_float(v[j]);
         } else {
           const uint32_t slot = src < q ? src : src - 1;
           const uint8_t* row = recv + slot * kF1SlotBytes + cl_row * 128;
 #pragma unroll
-          for (int ch = 0; ch < 8; ++ch) {
+          for (int c = 0; c < 4; ++c) {
+            const int ch = (c0 >> 2) + c;
             const float4 f = *reinterpret_cast<const float4*>(row + ((ch ^ (cl_row & 7)) << 4));
-            pv[4 * ch] = f.x;
-            pv[4 * ch + 1] = f.y;
-            pv[4 * ch + 2] = f.z;
-            pv[4 * ch + 3] = f.w;
+            pv[4 * c] = f.x;
+            pv[4 * c + 1] = f.y;
+            pv[4 * c + 2] = f.z;
+            pv[4 * c + 3] = f.w;
           }
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] = src == 0 ? pv[j] : z[j] + pv[j];
+        for (int j = 0; j < 16; ++j) z[j] = src == 0 ? pv[j] : z[j] + pv[j];
       }
-      named_bar_sync(2, 128);  // every thread has read the receive buffer
+      named_bar_sync(2, kE);  // every thread has read the receive buffer
       if (et < kF1KC && et != static_cast<int>(q)) mbar_arrive_remote(mapa_smem(xempty_s, et));
       if (a.bias != nullptr && valid) {
         const float bv = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(a.bias)[cls]);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] += bv;
+        for (int j = 0; j < 16; ++j) z[j] += bv;
       }
-      // ---- per-row tile max and top-1 class (ties -> lowest class): one redux per row
+      // ---- per-row tile max and top-1 class (ties -> lowest class): one redux per row; lane jj
+      //      keeps row c0 + jj's result (selects, no branches)
+      float my_m = -INFINITY;
+      int my_i = 0;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float zv = valid ? z[j] : -INFINITY;
+      for (int jj = 0; jj < 16; ++jj) {
+        const float zv = valid ? z[jj] : -INFINITY;
         const float m = redux_max_f32(zv);
         const unsigned hit = __ballot_sync(0xffffffffu, zv == m);
-        if (lane == j) {
-          red_v[qd][j] = m;
-          red_i[qd][j] = qd * 32 + __ffs(hit) - 1;
-        }
+        my_m = lane == jj ? m : my_m;
+        my_i = lane == jj ? static_cast<int>(__ffs(hit)) - 1 : my_i;
       }
-      named_bar_sync(2, 128);
+      if (lane < 16) {
+        red_v[qd][c0 + lane] = my_m;
+        red_i[qd][c0 + lane] = qd * 32 + my_i;
+      }
+      if (et == 0 && it >= 2) bulk_wait_read<1>();  // the P~ store of tile it - 2 has read its buffer
+      named_bar_sync(2, kE);
+      if (dbg) g_f1_ts[it * 16 + 8] = gtime_ns();
       if (et < 32) {
         float bm = red_v[0][et];
         int bi = red_i[0][et];
@@ -401,62 +454,93 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const float nref = move ? bm : old;
         s_fac[et] = (move && !first) ? exp2f((old - nref) * kL2e) : 1.f;
         s_ref[et] = nref;
-        s_c[et] = exp2f((nref - bm) * kL2e);  // exp(z - max) = exp(z - ref) * exp(ref - max)
         s_max[et] = bm;
         s_arg[et] = bi;
         const unsigned any = __ballot_sync(0xffffffffu, move && !first);
         if (et == 0) s_rescale = any != 0u;
       }
-      named_bar_sync(2, 128);
+      named_bar_sync(2, kE);
+      if (dbg) g_f1_ts[it * 16 + 9] = gtime_ns();
       // ---- U rescale when a reference moved: G2(it - 1) must have finished (G2(it) waits for
       //      this tile's pfull); then the P~ buffer of G2(it - 2) must be free
       if (s_rescale) {
         mbar_wait(&pempty[(it - 1) & 1], ((it - 1) >> 1) & 1);
         tc_fence_after();
         for (int m = 0; m < KQ / 2; ++m) {
-          uint32_t u[32];
-          const uint32_t ta = tmem_base + ucol0 + m * kF1NB + lane_off;
-          tmem_ld32(ta, u);
+          uint32_t u[16];
+          const uint32_t ta = tmem_base + ucol0 + m * kF1NB + c0 + lane_off;
+          tmem_ld16(ta, u);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) u[j] = __float_as_uint(__uint_as_float(u[j]) * s_fac[j]);
-          tmem_st32(ta, u);
+          for (int jj = 0; jj < 16; ++jj) u[jj] = __float_as_uint(__uint_as_float(u[jj]) * s_fac[c0 + jj]);
+          tmem_st16(ta, u);
         }
         tmem_st_wait();
       }
       if (it >= 2) mbar_wait(&pempty[it & 1], ((it >> 1) & 1) ^ 1u);
-      // ---- P~ (reference) -> G2 operand; P~ (tile max) -> global; s_tile; z_y
-      float ps[32];
-      uint8_t* prow = pbuf + (it & 1) * kF1PBytes + (cl_row >> 6) * (kF1NB * kRowBytes);
+      if (dbg) g_f1_ts[it * 16 + 10] = gtime_ns();
+      // ---- P~ = exp(z - ref) -> G2 operand (also the global P~ tile, stored by TMA); s_tile
+      float rf[16];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float4 r4 = *reinterpret_cast<const float4*>(&s_ref[c0 + 4 * c]);
+        rf[4 * c] = r4.x;
+        rf[4 * c + 1] = r4.y;
+        rf[4 * c + 2] = r4.z;
+        rf[4 * c + 3] = r4.w;
+      }
+      float ps[16];
+      uint8_t* pb = pbuf + (it & 1) * kF1PBytes;
+      uint8_t* prow = pb + (cl_row >> 6) * (kF1NB * kRowBytes);
       const int cb = (cl_row & 63) * 2;  // byte column within the 128-byte row
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float pr = valid ? ex2_approx((z[j] - s_ref[j]) * kL2e) : 0.f;
-        *reinterpret_cast<__nv_bfloat16*>(prow + j * 128 + ((((cb >> 4) ^ (j & 7)) << 4) | (cb & 15))) =
+      for (int jj = 0; jj < 16; ++jj) {
+        const int j = c0 + jj;
+        const float pr = valid ? ex2_approx((z[jj] - rf[jj]) * kL2e) : 0.f;
+        ps[jj] = pr;
+        *reinterpret_cast<__nv_bfloat16*>(prow + j * 128 + ((((cb >> 4) ^ (jj & 7)) << 4) | (cb & 15))) =
             __float2bfloat16_rn(pr);
-        const float pt = pr * s_c[j];
-        ps[j] = pt;
-        if (store_role && valid && j < a.Bt) {
-          a.P[static_cast<long long>(j) * a.ldp + cls] = __float2bfloat16_rn(pt);
-          if (static_cast<long long>(s_lab[j]) - a.class_offset == cls) a.zy[j] = z[j];
-        }
       }
+      if (store_role && valid) {  // the label logit (rows whose label falls in this tile)
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj)
+          if (c0 + jj < a.Bt && static_cast<long long>(s_lab[c0 + jj]) - a.class_offset == cls) a.zy[c0 + jj] = z[jj];
+      }
+      if (dbg) g_f1_ts[it * 16 + 11] = gtime_ns();
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&pfull[it & 1]);
-      if (dbg) g_f1_ts[it * 8 + 5] = gtime_ns();
-      f1_colsum32(ps, lane);
-      red_v[qd][lane] = ps[0];
-      named_bar_sync(2, 128);
+      if (dbg) g_f1_ts[it * 16 + 5] = gtime_ns();
+      // column sums over the warp's 32 class rows: lanes l and l ^ 16 first, then a transposed
+      // reduction over 16 columns -> lane l (< 16) holds column c0 + l
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj) ps[jj] += __shfl_xor_sync(0xffffffffu, ps[jj], 16);
+#pragma unroll
+      for (int w = 8; w >= 1; w >>= 1) {
+        const bool hi = (lane & w) != 0;
+#pragma unroll
+        for (int i = 0; i < w; ++i) {
+          const float sv = hi ? ps[i] : ps[i + w];
+          const float kv = hi ? ps[i + w] : ps[i];
+          ps[i] = kv + __shfl_xor_sync(0xffffffffu, sv, w);
+        }
+      }
+      if (lane < 16) red_v[qd][c0 + lane] = ps[0];
+      named_bar_sync(2, kE);
+      if (et == 0) {  // this CTA's 64-class half of the P~ tile -> global (rows >= B_tot clipped)
+        tma_store_2d(&tmP, pb + q * (kF1NB * kRowBytes), t * kF1TileC + static_cast<int>(q) * 64, 0);
+        bulk_commit();
+      }
       if (q == 0 && et < a.Bt) {
         const float s = (red_v[0][et] + red_v[1][et]) + (red_v[2][et] + red_v[3][et]);
         const size_t o = static_cast<size_t>(et) * a.num_tiles + t;
-        a.m_tile[o] = s_max[et];
+        a.m_tile[o] = s_ref[et];  // P~ and s_tile are relative to the reference
         a.s_tile[o] = s;
+        a.mx_tile[o] = s_max[et];  // true tile max (predictions)
         if (a.a_tile) a.a_tile[o] = static_cast<int32_t>(a.class_offset + static_cast<long long>(t) * kF1TileC + s_arg[et]);
       }
-      named_bar_sync(2, 128);  // red_v is reused by the next tile
-      if (dbg) g_f1_ts[it * 8 + 6] = gtime_ns();
+      named_bar_sync(2, kE);  // red_v is reused by the next tile
+      if (dbg) g_f1_ts[it * 16 + 6] = gtime_ns();
     }
     // ---- this CTA's part of U (relative to s_ref) -> global partials
     const size_t ubase = static_cast<size_t>(cl) * a.Bt;
@@ -465,23 +549,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
     }
     for (int m = 0; m < KQ / 2; ++m) {
-      uint32_t u[32];
+      uint32_t u[16];
       if (my_tiles > 0) {
-        tmem_ld32(tmem_base + ucol0 + m * kF1NB + lane_off, u);
+        tmem_ld16(tmem_base + ucol0 + m * kF1NB + c0 + lane_off, u);
         tmem_ld_wait();
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) u[j] = 0u;
+        for (int jj = 0; jj < 16; ++jj) u[jj] = 0u;
       }
       const int d = d0 + m * 128 + cl_row;
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < a.Bt) __stcg(a.upart + (ubase + j) * a.D + d, __uint_as_float(u[j]));
+      for (int jj = 0; jj < 16; ++jj)
+        if (c0 + jj < a.Bt) __stcg(a.upart + (ubase + c0 + jj) * a.D + d, __uint_as_float(u[jj]));
     }
     if (q == 0 && et < a.Bt) a.uref[ubase + et] = s_ref[et];
+    if (et == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
+  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) g_f1_cta[blockIdx.x * 3 + 2] = gtime_ns();
   cluster_sync();  // no CTA leaves while a peer may still write into its shared memory
   if (warp == 2) {
     tc_fence_after();

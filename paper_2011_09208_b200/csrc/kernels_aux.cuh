@@ -127,6 +127,7 @@ struct StatsArgs {
   int grad_vecs;         // 16-byte vectors of P~ per thread in the fused gradient (chunk size)
   // NEXT-4 predictions (optional): top-1 class of each local row and its probability
   const int32_t* a_tile; // [Bt x T] argmax class per (row, tile) from the logits epilogue
+  const float* mx_tile;  // [Bt x T] true tile maxima when m_tile holds references (F1), else NULL
   int32_t* pred_local;   // [B] or NULL
   float* prob_local;     // [B] or NULL
 };
@@ -310,6 +311,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
   const int i = blockIdx.y;
   const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
   const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
+  const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : mt;  // true maxima
   float mloc[8], sloc[8];
   float m = -INFINITY;
 #pragma unroll
@@ -317,9 +319,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
     const int t = threadIdx.x + k * kStatsThreads;
     mloc[k] = t < a.T ? __ldg(mt + t) : -INFINITY;
     sloc[k] = t < a.T ? __ldg(st + t) : 0.f;
-    m = fmaxf(m, mloc[k]);
+    m = fmaxf(m, t < a.T ? __ldg(mx + t) : -INFINITY);
   }
-  for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, __ldg(mt + t));
+  for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, __ldg(mx + t));
   m = block_max128(m, red);
   float s = 0.f;
 #pragma unroll
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
   }
   if (a.pred_local != nullptr && blockIdx.x == 0) {  // top-1: first tile holding the row max
     __shared__ int redi[4];
-    const int ts = argmax_tile(mt, a.T, m, redi);
+    const int ts = argmax_tile(mx, a.T, m, redi);
     if (threadIdx.x == 0) {
       a.pred_local[i] = a.a_tile[static_cast<size_t>(i) * a.T + ts];
       if (a.prob_local) a.prob_local[i] = 1.f / s;  // e^{m - lse}
@@ -415,6 +417,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
   if (tslot >= 0) g_dbg_ts[tslot] = gtime_ns();
   const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
   const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
+  const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : mt;  // true maxima
   const long long y = a.y[i];
   const long long yl = y - a.o_r;
   if (chunk_id == 0) {
@@ -425,9 +428,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
       const int t = threadIdx.x + k * kStatsThreads;
       mloc[k] = t < a.T ? __ldg(mt + t) : -INFINITY;
       sloc[k] = t < a.T ? __ldg(st + t) : 0.f;
-      m = fmaxf(m, mloc[k]);
+      m = fmaxf(m, t < a.T ? __ldg(mx + t) : -INFINITY);
     }
-    for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, __ldg(mt + t));
+    for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, __ldg(mx + t));
     m = block_max128(m, red);
     float s = 0.f;
 #pragma unroll
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
     s = block_sum128(s, red);
     if (tslot >= 0) g_dbg_ts[tslot + 1] = gtime_ns();
     __shared__ int redi[4];
-    const int top = argmax_tile(mt, a.T, m, redi);  // this rank's top-1 tile for the row
+    const int top = argmax_tile(mx, a.T, m, redi);  // this rank's top-1 tile for the row
     const int top_class = a.a_tile[static_cast<size_t>(i) * a.T + top];
     if (threadIdx.x < a.world) {  // thread p pushes the record to peer p
       if (threadIdx.x == 0 && (y < 0 || y >= a.C)) atomicOr(a.err, ERR_LABEL);

@@ -185,6 +185,7 @@ struct Layout {
   size_t P = 0, m_tile = 0, s_tile = 0, zy = 0, lse = 0, row_loss = 0, dxpart = 0, counters = 0, tile_cnt = 0;
   size_t a_tile = 0, dbpart = 0;  // NEXT-4: per-(row, tile) top-1 class; bias-gradient partials
   size_t upart = 0, uref = 0;     // F1: per-cluster U = sum_t P~_t W_t partials and their row references
+  size_t mx_tile = 0;             // F1: true per-(row, tile) maxima (m_tile holds the references)
   size_t local_total = 0;
   // fp32 (kind::tf32) backward only: K-major transposed operands
   size_t XT = 0, GT = 0, WT = 0;
@@ -372,7 +373,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
       // stages: provisional here (host-only planning); create() sizes them with the kernel's
       // real static shared memory
       const int fixed = f1_smem_bytes(0, p.f1_Dq) + 2048;
-      p.f1_stages = std::min(8, (kSmemLimit - fixed) / kF1StageBytes) & ~1;
+      p.f1_stages = std::min(8, (kSmemLimit - fixed) / kF1G1SlotBytes);
       p.f1_smem = f1_smem_bytes(p.f1_stages, p.f1_Dq);
       if (p.f1_stages < 4) p.f1 = false;
     }
@@ -404,6 +405,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   if (p.f1) {
     L.upart = take(static_cast<size_t>(p.f1_ncl) * p.Bt * p.D * 4);
     L.uref = take(static_cast<size_t>(p.f1_ncl) * p.Bt * 4);
+    L.mx_tile = take(static_cast<size_t>(p.Bt) * p.fwd.n_blocks * 4);
   }
   if (p.es == 4) {
     L.ld_bt = static_cast<int64_t>(align_up(p.Bt, 4));
@@ -517,7 +519,7 @@ struct whale_splitfc_ctx {
   // pointer-cached maps
   const void* x_cached = nullptr;
   const void* w_cached = nullptr;
-  CUtensorMap tmW_fwd, tmW_dx, tmW_f1, tmX_f1;
+  CUtensorMap tmW_fwd, tmW_dx, tmW_f1, tmX_f1, tmP_f1;
   const void* dw_cached = nullptr;
   CUtensorMap tmDW;
   const void* x_fwd = nullptr;       // N = 1: the forward's X (read again by dW)
@@ -696,7 +698,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     cudaFuncAttributes fa{};
     CUDA_TRY(cudaFuncGetAttributes(&fa, splitfc_fwd_dx_kernel));
     const int fixed = f1_smem_bytes(0, p.f1_Dq) + static_cast<int>(fa.sharedSizeBytes);
-    c->p.f1_stages = std::min(8, (kSmemLimit - fixed) / kF1StageBytes) & ~1;
+    c->p.f1_stages = std::min(8, (kSmemLimit - fixed) / kF1G1SlotBytes);
     c->p.f1_smem = f1_smem_bytes(c->p.f1_stages, p.f1_Dq);
     if (c->p.f1_stages < 4) {
       delete c;
@@ -706,7 +708,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
                                   kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(c->p.f1_ncl * kF1KC);
-    cfg.blockDim = dim3(kGemmThreads);
+    cfg.blockDim = dim3(kF1Threads);
     cfg.dynamicSmemBytes = p.f1_smem;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -735,6 +737,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   }
   void* P = c->ws + p.L.P;
   MAP_TRY(map2d(&c->tmP_store, P, es, p.Cr, p.Bt, p.ldp * es, kRowBytes / es, 32));
+  if (p.f1) MAP_TRY(map2d(&c->tmP_f1, P, es, p.Cr, p.Bt, p.ldp * es, 64, kF1NB));
   MAP_TRY(map2d(&c->tmG_dx, P, es, p.Cr, p.Bt, p.ldp * es, kbk, kBM));
   MAP_TRY(map2d(&c->tmG_dw, P, es, p.Cr, p.Bt, p.ldp * es, atom, p.dw.bk));
   MAP_TRY(map3d_f32(&c->tmDxPart, c->ws + p.L.dxpart, p.D, p.Bt, p.dx.splits));
@@ -861,8 +864,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.s_tile = wsp<float>(c, L.s_tile);
     a.zy = wsp<float>(c, L.zy);
     a.a_tile = wsp<int32_t>(c, L.a_tile);
-    a.P = wsp<__nv_bfloat16>(c, L.P);
-    a.ldp = p.ldp;
+    a.mx_tile = wsp<float>(c, L.mx_tile);
     a.upart = wsp<float>(c, L.upart);
     a.uref = wsp<float>(c, L.uref);
     a.dev_epoch = dev_epoch;
@@ -875,7 +877,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.f1_ncl * kF1KC);
-    cfg.blockDim = dim3(kGemmThreads);
+    cfg.blockDim = dim3(kF1Threads);
     cfg.dynamicSmemBytes = p.f1_smem;
     cfg.stream = s;
     cudaLaunchAttribute at[2];
@@ -888,7 +890,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     cfg.attrs = at;
     cfg.numAttrs = c->pdl ? 2 : 1;
     PROFILED(K_LOGITS, s, ([&]() -> whale_status_t {
-               CUDA_TRY(cudaLaunchKernelEx(&cfg, splitfc_fwd_dx_kernel, c->tmW_f1, c->tmX_f1, a));
+               CUDA_TRY(cudaLaunchKernelEx(&cfg, splitfc_fwd_dx_kernel, c->tmW_f1, c->tmX_f1, c->tmP_f1, a));
                return WHALE_OK;
              }()));
   } else {
@@ -945,6 +947,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     // every CTA re-reads its row's T tile partials (8T bytes): size the chunk so that this
     // stays <= ~10% of the chunk's P~ read+write traffic (4096 B per vector of the 128 threads)
     a.a_tile = wsp<int32_t>(c, L.a_tile);
+    a.mx_tile = p.f1 ? wsp<float>(c, L.mx_tile) : nullptr;
     a.pred_local = pred;
     a.prob_local = prob;
     a.grad_vecs = static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(4, (p.fwd.n_blocks * 10 + 511) / 512)));
@@ -1311,7 +1314,7 @@ extern "C" int whale_debug_f1_max_clusters(int smem) {
     return -2;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(148);
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(kF1Threads);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1325,8 +1328,9 @@ extern "C" int whale_debug_f1_max_clusters(int smem) {
   return n;
 }
 
-// Internal: read the F1 debug timeline (64 periods x 8 stamps, ns).  Synchronises the device.
+// Internal: read the F1 debug timeline (64 periods x 16 stamps, then 160 CTAs x {entry, start, end}, ns).  Synchronises the device.
 extern "C" int whale_debug_f1_timeline(unsigned long long* out) {
   if (cudaDeviceSynchronize() != cudaSuccess) return -1;
-  return cudaMemcpyFromSymbol(out, g_f1_ts, sizeof(g_f1_ts)) == cudaSuccess ? 0 : -2;
+  if (cudaMemcpyFromSymbol(out, g_f1_ts, sizeof(g_f1_ts)) != cudaSuccess) return -2;
+  return cudaMemcpyFromSymbol(out + 1024, g_f1_cta, sizeof(g_f1_cta)) == cudaSuccess ? 0 : -3;
 }

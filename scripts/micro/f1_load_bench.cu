@@ -15,12 +15,47 @@ __global__ void __launch_bounds__(128, 1) f1_load_kernel(const __grid_constant__
                                                          int mode, int* sink) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* base = sm + ((1024 - (smem_u32(sm) & 1023)) & 1023);
-  __shared__ uint64_t full[16];
+  __shared__ uint64_t full[16], empty[16];
   if (threadIdx.x == 0) {
-    for (int i = 0; i < stages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
     fence_mbar_init();
   }
   __syncthreads();
+  if (mode & 2) {  // producer (thread 0) / consumer (thread 32) handoff through empty barriers
+    const int stage_bytes = 128 * 128;
+    const int tiles = (C + 127) / 128;
+    int q = 0, cl = blockIdx.x, ncl = gridDim.x, kb0 = 0, kb1 = D / 64;
+    if (mode & 1) {
+      q = cluster_ctarank();
+      cl = cluster_id_x();
+      ncl = ncluster_x();
+      kb0 = q * (D / 128);
+      kb1 = kb0 + D / 128;
+    }
+    int n = 0;
+    for (int t = cl; t < tiles; t += ncl) n += kb1 - kb0;
+    if (threadIdx.x == 0) {
+      int s = 0; uint32_t ph = 0, i = 0;
+      for (int t = cl; t < tiles; t += ncl)
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          tma_load_2d(base + s * stage_bytes, &map, &full[s], kb * 64, t * 128);
+          if (++s == stages) { s = 0; ph ^= 1u; }
+        }
+    } else if (threadIdx.x == 32) {
+      int s = 0; uint32_t ph = 0;
+      for (int i = 0; i < n; ++i) {
+        mbar_wait(&full[s], ph);
+        mbar_arrive(&empty[s]);
+        if (++s == stages) { s = 0; ph ^= 1u; }
+      }
+    }
+    return;
+  }
   if (threadIdx.x != 0) return;
   const int stage_bytes = 128 * 128;
   const int tiles = (C + 127) / 128;
@@ -74,7 +109,7 @@ int main() {
     cuuint32_t bd[2] = {64, 128}, es[2] = {1, 1};
     enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, gd, gs, bd, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, prom, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    for (int mode : {0, 1}) {
+    for (int mode : {0, 1, 3}) {
       for (int stages : {4, 8, 12}) {
         int smem = stages * 128 * 128 + 1024;
         cudaLaunchConfig_t cfg{};
