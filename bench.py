@@ -373,8 +373,8 @@ def kernel_work(name, cfgj, cfg, es):
         return bx + bw, fx + fw
     if name == "softmax_grad":  # read + write P~/G in place, read tile maxima
         return 2 * Bt * Cr * es + Bt * T * 4, 0
-    if name == "stats_combine":
-        return 2 * Bt * T * 4 + Bt * 16 * world, 0
+    if name == "stats_combine":  # tile partials (+ true maxima for F1) + the fused in-place G rewrite
+        return (3 if f1 else 2) * Bt * T * 4 + Bt * 16 * world + 2 * Bt * Cr * es, 0
     if name == "bridge_gather":
         return B * D * es * (1 + world), 0
     if name == "dx_rs_push":
