@@ -300,6 +300,50 @@ __global__ void __launch_bounds__(256) softmax_grad_kernel(void* P, long long ld
 // G = (P~ e^{m_tile - lse} - onehot) / B_tot in place, chunk 0 writes lse / row loss, and
 // the last CTA sums the mean loss in a fixed order.
 constexpr int kGradVecs = 4;  // 16-byte vectors per thread
+// G_r[i, j] = P~[i, j] * e^{m_tile(i, j / BN) - lse_i} / B_tot - [j == y_i] / B_tot, in place over
+// this CTA's chunk of row i.  Loads are issued kU vectors at a time before any store (the
+// stores may alias later loads as far as the compiler knows, so a plain loop serialises
+// load -> store round trips).
+template <int ES>
+__device__ __forceinline__ void grad_rewrite(const StatsArgs& a, void* P, long long ldp, int BN, float inv_bt, int i,
+                                             int chunk_id, const float* mt, float l, long long yl) {
+  constexpr int V = 16 / ES;
+  constexpr int kU = 4;
+  const long long chunk = static_cast<long long>(kStatsThreads) * a.grad_vecs * V;
+  for (int k0 = 0; k0 < a.grad_vecs; k0 += kU) {
+    uint4 raw[kU];
+    long long j0s[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      j0s[u] = chunk_id * chunk + (static_cast<long long>(k0 + u) * kStatsThreads + threadIdx.x) * V;
+      if (k0 + u < a.grad_vecs && j0s[u] < a.C_r)
+        raw[u] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(P) + (i * ldp + j0s[u]) * ES);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long j0 = j0s[u];
+      if (k0 + u >= a.grad_vecs || j0 >= a.C_r) continue;
+      const float scale = __expf(__ldg(mt + j0 / BN) - l) * inv_bt;
+      if constexpr (ES == 2) {
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw[u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 f = __bfloat1622float2(h[q]);
+          const long long j = j0 + 2 * q;
+          f.x = f.x * scale - ((j == yl) ? inv_bt : 0.f);
+          f.y = f.y * scale - ((j + 1 == yl) ? inv_bt : 0.f);
+          h[q] = __floats2bfloat162_rn(f.x, f.y);
+        }
+      } else {
+        float* f = reinterpret_cast<float*>(&raw[u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) f[q] = f[q] * scale - ((j0 + q == yl) ? inv_bt : 0.f);
+      }
+      *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(P) + (i * ldp + j0) * ES) = raw[u];
+    }
+  }
+}
+
 template <int ES>
 __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsArgs a, void* P, long long ldp,
                                                                    int BN, float inv_bt) {
@@ -348,35 +392,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
     }
   }
   // ---- G for this CTA's chunk of the row
-  const long long chunk = static_cast<long long>(kStatsThreads) * a.grad_vecs * V;
-#pragma unroll 4
-  for (int k = 0; k < a.grad_vecs; ++k) {
-    const long long j0 = blockIdx.x * chunk + (static_cast<long long>(k) * kStatsThreads + threadIdx.x) * V;
-    if (j0 >= a.C_r) break;
-    const float scale = __expf(__ldg(mt + j0 / BN) - l) * inv_bt;
-    if constexpr (ES == 2) {
-      uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P) + i * ldp + j0);
-      uint4 raw = *p;
-      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float2 f = __bfloat1622float2(h[q]);
-        const long long j = j0 + 2 * q;
-        f.x = f.x * scale - ((j == yl) ? inv_bt : 0.f);
-        f.y = f.y * scale - ((j + 1 == yl) ? inv_bt : 0.f);
-        h[q] = __floats2bfloat162_rn(f.x, f.y);
-      }
-      *p = raw;
-    } else {
-      float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(P) + i * ldp + j0);
-      float4 f = *p;
-      f.x = f.x * scale - ((j0 == yl) ? inv_bt : 0.f);
-      f.y = f.y * scale - ((j0 + 1 == yl) ? inv_bt : 0.f);
-      f.z = f.z * scale - ((j0 + 2 == yl) ? inv_bt : 0.f);
-      f.w = f.w * scale - ((j0 + 3 == yl) ? inv_bt : 0.f);
-      *p = f;
-    }
-  }
+  grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, blockIdx.x, mt, l, yl);
   // ---- mean loss: last CTA, fixed order
   if (blockIdx.x != 0 || !last_of_n(a.counter, gridDim.y)) return;  // loss: chunk-0 CTAs only
   double acc = 0.0;
@@ -493,35 +509,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
     if (a.row_loss_local && i >= a.row0 && i < a.row0 + a.B) a.row_loss_local[i - a.row0] = l - zz;
   }
   // ---- G for this CTA's chunk of the row
-  const long long chunk = static_cast<long long>(kStatsThreads) * a.grad_vecs * V;
-#pragma unroll 4
-  for (int k = 0; k < a.grad_vecs; ++k) {
-    const long long j0 = chunk_id * chunk + (static_cast<long long>(k) * kStatsThreads + threadIdx.x) * V;
-    if (j0 >= a.C_r) break;
-    const float scale = __expf(__ldg(mt + j0 / BN) - l) * inv_bt;
-    if constexpr (ES == 2) {
-      uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P) + i * ldp + j0);
-      uint4 raw = *p;
-      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float2 f = __bfloat1622float2(h[q]);
-        const long long j = j0 + 2 * q;
-        f.x = f.x * scale - ((j == yl) ? inv_bt : 0.f);
-        f.y = f.y * scale - ((j + 1 == yl) ? inv_bt : 0.f);
-        h[q] = __floats2bfloat162_rn(f.x, f.y);
-      }
-      *p = raw;
-    } else {
-      float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(P) + i * ldp + j0);
-      float4 f = *p;
-      f.x = f.x * scale - ((j0 == yl) ? inv_bt : 0.f);
-      f.y = f.y * scale - ((j0 + 1 == yl) ? inv_bt : 0.f);
-      f.z = f.z * scale - ((j0 + 2 == yl) ? inv_bt : 0.f);
-      f.w = f.w * scale - ((j0 + 3 == yl) ? inv_bt : 0.f);
-      *p = f;
-    }
-  }
+  grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, chunk_id, mt, l, yl);
   if (chunk_id != 0 || !last_of_n(a.counter, gridDim.x)) return;  // loss: chunk-0 CTAs only
   double acc = 0.0;
   for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) acc += static_cast<double>(__ldcg(a.row_loss_all + r));

@@ -685,8 +685,9 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   c->pdl = !(pdl_env && pdl_env[0] == '0');
   c->fused_bwd = p.es == 2 && env_int("WHALE_FUSED_BWD", 1) != 0 && g_store_mode == 1;
   if (c->fused_bwd) {
-    c->bwd_stage_bytes = std::max(p.dx.stage_bytes, p.dw.stage_bytes);
-    c->bwd_epi_bufs = 4;  // CTA-wide 16 KB store stages
+    // F1: the backward runs dW tiles only (dX came from the forward)
+    c->bwd_stage_bytes = p.f1 ? p.dw.stage_bytes : std::max(p.dx.stage_bytes, p.dw.stage_bytes);
+    c->bwd_epi_bufs = env_int("WHALE_BWD_EPI", p.f1 ? 8 : 4);  // CTA-wide 16 KB store stages (dW-only: deeper)
     const int fixed = 1024 + 512 + c->bwd_epi_bufs * 4 * kEpiBufBytes;
     c->bwd_stages = std::min(8, (kSmemLimit - kStaticSmemSlack - fixed) / c->bwd_stage_bytes);
     c->bwd_smem = fixed + c->bwd_stages * c->bwd_stage_bytes;
