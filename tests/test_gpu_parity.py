@@ -116,8 +116,8 @@ def test_parity_tiny_fp32(whale):
     (kind::tf32, DESIGN.md R11), single-GPU view of the whole global batch."""
     cfg = syn.CONFIGS["tiny"]
     seed = syn.config_seed("tiny", 2)
-    Bt = cfg.B * 2
-    for regime in ("init", "peaked"):
+    # R11 reading (B per rank -> B_tot = 16) and the alternative reading B_tot = 8 (SURVEY 8(c).11)
+    for Bt, regime in ((cfg.B * 2, "init"), (cfg.B * 2, "peaked"), (cfg.B, "init"), (cfg.B, "peaked")):
         X = syn.gen_features((0, Bt), cfg.D, seed, "f32")
         W = syn.gen_weight((0, cfg.C), cfg.D, seed, regime, "f32")
         y = syn.gen_labels((0, Bt), cfg.C, seed)
@@ -126,7 +126,7 @@ def test_parity_tiny_fp32(whale):
         # per-row loss under tf32: both operands rounded to 10+1 mantissa bits (u = 2^-11)
         # -> |dz| <~ 2u * sum_k |x_k w_k|, i.e. ~1e-3 relative on |z| ~ 20-30 in the peaked
         # regime; DESIGN.md "Tolerances" derives row_rtol = 5e-3 (mean loss keeps 1e-3).
-        _check_full(g, f, f"tiny/{regime}", row_rtol=5e-3)
+        _check_full(g, f, f"tiny/B_tot={Bt}/{regime}", row_rtol=5e-3)
 
 
 def test_labels_on_edges(whale):
