@@ -3,11 +3,12 @@
 //   bridge_gather_kernel   A2  all-gather of X_r, y_r into every rank's gathered buffer
 //                              (one-sided NVLink stores + release flags); N > 1 only -- at
 //                              N = 1 the GEMMs read the caller's X directly
-//   stats_rows_kernel      A4+A5  one CTA per row: (m_r, s_r, z_y,r) over the class tiles;
-//                              N > 1: push the float4 to every peer; the last CTA combines
-//                              in rank order (lse, per-row loss) and sums the mean loss in a
-//                              fixed order -> identical bits on every rank
-//   softmax_grad_kernel    A6  G = (P~ e^{m_tile - lse} - onehot) / B_tot, in place
+//   stats_grad_kernel      A4-A6 (N = 1): lse from the class-tile partials, loss, and
+//                              G = (P~ e^{m_tile - lse} - onehot) / B_tot in place
+//   stats_grad_multi_kernel A4-A6 (N > 1): the same with the per-row (m_r, s_r, z_y,r, top-1)
+//                              exchange as LL words over NVLink; rank-order combine ->
+//                              identical loss bits on every rank
+//   bias_grad_*_kernel     NEXT-4 db_r = column sums of G_r (two fixed-order passes)
 //   dx_reduce_kernel       A8  owner side of the dX reduce-scatter: wait for the peers'
 //                              pushes (done by the dX GEMM's fused fixup), sum in rank order
 //   transpose_f32_kernel       fp32 (kind::tf32) backward only: K-major operand copies
@@ -167,130 +168,6 @@ __device__ __forceinline__ float block_sum128(float v, float* red) {
   const float r = (red[0] + red[1]) + (red[2] + red[3]);
   __syncthreads();
   return r;
-}
-
-// One CTA (128 threads) per row: all of the row's tile partials are loaded at once
-// (latency-bound otherwise), then s = sum_t s_t e^{m_t - m} (online-softmax combine).
-template <bool kMulti>
-__global__ void __launch_bounds__(kStatsThreads) stats_rows_kernel(const StatsArgs a) {
-  __shared__ float red[4];
-  pdl_wait();
-  pdl_trigger();
-  TraceScope _trace(2);
-  const int i = blockIdx.x;
-  const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
-  const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
-  float mloc[8], sloc[8];
-  float m = -INFINITY;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int t = threadIdx.x + k * kStatsThreads;
-    mloc[k] = t < a.T ? mt[t] : -INFINITY;
-    sloc[k] = t < a.T ? st[t] : 0.f;
-    m = fmaxf(m, mloc[k]);
-  }
-  for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, mt[t]);
-  m = block_max128(m, red);
-  float s = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s += sloc[k] * __expf(mloc[k] - m);
-  for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) s += st[t] * __expf(mt[t] - m);
-  s = block_sum128(s, red);
-  if (threadIdx.x == 0) {
-    const long long y = a.y[i];
-    if (y < 0 || y >= a.C) atomicOr(a.err, ERR_LABEL);
-    const bool own = (y >= a.o_r) && (y < a.o_r + a.C_r);
-    const float zy = own ? a.zy_r[i] : 0.f;
-    if constexpr (!kMulti) {
-      const float l = m + logf(s);
-      a.lse[i] = l;
-      a.row_loss_all[i] = l - zy;
-      if (a.row_loss_local) a.row_loss_local[i] = l - zy;
-    } else {
-      const float4 rec = make_float4(m, s, zy, 0.f);
-      for (int p = 0; p < a.world; ++p)
-        reinterpret_cast<float4*>(a.peer_stats.p[p])[static_cast<size_t>(a.rank) * a.Bt + i] = rec;
-    }
-  }
-  if (!last_block_ticket<kMulti>(a.counter)) return;
-  // ---- last CTA: (N > 1) exchange + rank-ordered combine; fixed-order mean loss ----
-  if constexpr (kMulti) {
-    const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;
-    if (threadIdx.x < a.world) st_release_sys(a.peer_flags.p[threadIdx.x], e);
-    if (threadIdx.x < a.world) wait_flag_geq(a.my_flags + threadIdx.x, e, a.err, ERR_COMM);
-    __syncthreads();
-    __threadfence_system();
-    for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) {
-      float mm = -INFINITY;
-      for (int p = 0; p < a.world; ++p) mm = fmaxf(mm, a.my_stats[static_cast<size_t>(p) * a.Bt + r].x);
-      float ss = 0.f, zz = 0.f;
-      for (int p = 0; p < a.world; ++p) {
-        const float4 rec = a.my_stats[static_cast<size_t>(p) * a.Bt + r];
-        ss += rec.y * __expf(rec.x - mm);
-        zz += rec.z;  // exactly one rank owns the label; the others contribute 0
-      }
-      const float l = mm + logf(ss);
-      a.lse[r] = l;
-      a.row_loss_all[r] = l - zz;
-      if (a.row_loss_local && r >= a.row0 && r < a.row0 + a.B) a.row_loss_local[r - a.row0] = l - zz;
-    }
-    __syncthreads();
-  }
-  double acc = 0.0;
-  for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) acc += static_cast<double>(__ldcg(a.row_loss_all + r));
-  __shared__ double part[4];
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *a.loss = static_cast<float>(((part[0] + part[1]) + (part[2] + part[3])) / a.Bt);
-    *a.counter = 0;
-  }
-}
-
-// ---------------------------------------------------------------- A6 gradient
-// G[i, j] = (P~[i, j] * exp(m_tile[i, j / BN] - lse_i) - [j == y_i - o_r]) / B_tot, in place.
-// One thread per 8 (bf16) / 4 (fp32) consecutive classes of one row (16-byte vectors).
-template <int ES>
-__global__ void __launch_bounds__(256) softmax_grad_kernel(void* P, long long ldp, int Bt, long long C_r, int BN,
-                                                           int T, const float* __restrict__ m_tile,
-                                                           const float* __restrict__ lse,
-                                                           const int32_t* __restrict__ y, long long o_r,
-                                                           float inv_bt) {
-  constexpr int V = 16 / ES;
-  pdl_wait();
-  pdl_trigger();
-  TraceScope _trace(3);
-  const int i = blockIdx.y;
-  const long long j0 = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * V;
-  if (j0 >= C_r) return;
-  const float l = lse[i];
-  const long long yl = static_cast<long long>(y[i]) - o_r;
-  const float* mt = m_tile + static_cast<size_t>(i) * T;
-  // BN is a multiple of V, so the V classes share one tile scale
-  const float scale = __expf(mt[j0 / BN] - l) * inv_bt;
-  if constexpr (ES == 2) {
-    uint4* p = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P) + i * ldp + j0);
-    uint4 raw = *p;
-    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float2 f = __bfloat1622float2(h[k]);
-      const long long j = j0 + 2 * k;
-      f.x = f.x * scale - ((j == yl) ? inv_bt : 0.f);
-      f.y = f.y * scale - ((j + 1 == yl) ? inv_bt : 0.f);
-      h[k] = __floats2bfloat162_rn(f.x, f.y);
-    }
-    *p = raw;
-  } else {
-    float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(P) + i * ldp + j0);
-    float4 f = *p;
-    f.x = f.x * scale - ((j0 == yl) ? inv_bt : 0.f);
-    f.y = f.y * scale - ((j0 + 1 == yl) ? inv_bt : 0.f);
-    f.z = f.z * scale - ((j0 + 2 == yl) ? inv_bt : 0.f);
-    f.w = f.w * scale - ((j0 + 3 == yl) ? inv_bt : 0.f);
-    *p = f;
-  }
 }
 
 // ---------------------------------------------------------------- A4-A6 fused (N = 1)

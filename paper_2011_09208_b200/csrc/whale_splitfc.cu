@@ -1028,18 +1028,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     if (st != WHALE_OK) return st;
     c->dw_cached = dw;
   }
-  // ---- A6 G = (softmax - onehot) / B_tot is produced by the forward's fused stats kernel;
-  //      the standalone kernel remains for WHALE_SPLIT_GRAD experiments only.
-  if (false) {
-    constexpr int V = 16 / ES;
-    dim3 grid(cdiv(cdiv(p.Cr, V), 256), static_cast<unsigned>(p.Bt));
-    PROFILED(K_GRAD, s,
-             (launch(c, softmax_grad_kernel<ES>, grid, dim3(256), 0, s, static_cast<void*>(c->ws + L.P),
-                     static_cast<long long>(p.ldp), static_cast<int>(p.Bt), static_cast<long long>(p.Cr),
-                     p.fwd.BN, p.fwd.n_blocks, static_cast<const float*>(wsp<float>(c, L.m_tile)),
-                     static_cast<const float*>(wsp<float>(c, L.lse)), yg, static_cast<long long>(p.o_r),
-                     static_cast<float>(1.0 / static_cast<double>(p.Bt)))));
-  }
+  // ---- A6 G = (softmax - onehot) / B_tot was produced by the forward's fused stats kernel
   // ---- NEXT-4 bias gradient db_r = sum_i G_r[i, :] (fixed row order, two passes)
   if (db != nullptr) {
     constexpr int V = 16 / ES;
