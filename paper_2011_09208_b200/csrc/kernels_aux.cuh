@@ -181,6 +181,34 @@ constexpr int kGradVecs = 4;  // 16-byte vectors per thread
 // this CTA's chunk of row i.  Loads are issued kU vectors at a time before any store (the
 // stores may alias later loads as far as the compiler knows, so a plain loop serialises
 // load -> store round trips).
+constexpr int kRowWriter = 32;  // thread that writes a row's lse / loss (warp 1: no peer stores)
+
+// Mean loss over the global batch: every row's chunk-0 CTA takes a ticket after writing its
+// row loss; the last one sums the B_tot row losses in a fixed order (identical bits on every
+// rank) and re-arms the counter.
+__device__ __forceinline__ void mean_loss_ticket(const StatsArgs& a) {
+  // only the row-result writer fences (a GPU-scope fence by a thread that just stored to a
+  // peer over NVLink would wait for those remote stores)
+  __shared__ bool is_last;
+  if (threadIdx.x == kRowWriter) {
+    __threadfence();
+    is_last = atomicAdd(a.counter, 1u) == static_cast<unsigned>(a.Bt) - 1u;
+    if (is_last) __threadfence();
+  }
+  __syncthreads();
+  if (!is_last) return;
+  double acc = 0.0;
+  for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) acc += static_cast<double>(__ldcg(a.row_loss_all + r));
+  __shared__ double part[4];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *a.loss = static_cast<float>(((part[0] + part[1]) + (part[2] + part[3])) / a.Bt);
+    *a.counter = 0;
+  }
+}
+
 template <int ES>
 __device__ __forceinline__ void grad_rewrite(const StatsArgs& a, void* P, long long ldp, int BN, float inv_bt, int i,
                                              int chunk_id, const float* mt, float l, long long yl) {
@@ -252,7 +280,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
   const float l = m + logf(s);
   const long long y = a.y[i];
   const long long yl = y - a.o_r;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == kRowWriter) {
     if (y < 0 || y >= a.C) atomicOr(a.err, ERR_LABEL);
     const bool own = (y >= a.o_r) && (y < a.o_r + a.C_r);
     const float zy = own ? a.zy_r[i] : 0.f;
@@ -268,20 +296,10 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
       if (a.prob_local) a.prob_local[i] = 1.f / s;  // e^{m - lse}
     }
   }
+  // ---- mean loss (chunk-0 CTAs, before their G chunk): the last one sums all rows in order
+  if (blockIdx.x == 0) mean_loss_ticket(a);
   // ---- G for this CTA's chunk of the row
   grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, blockIdx.x, mt, l, yl);
-  // ---- mean loss: last CTA, fixed order
-  if (blockIdx.x != 0 || !last_of_n(a.counter, gridDim.y)) return;  // loss: chunk-0 CTAs only
-  double acc = 0.0;
-  for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) acc += static_cast<double>(__ldcg(a.row_loss_all + r));
-  __shared__ double part[4];
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *a.loss = static_cast<float>(((part[0] + part[1]) + (part[2] + part[3])) / a.Bt);
-    *a.counter = 0;
-  }
 }
 
 // ---------------------------------------------------------------- A4-A6 fused (N > 1)
@@ -380,24 +398,20 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
     a.pred_local[i - a.row0] = static_cast<int32_t>(__float_as_uint(recs[top_rank].w));
     if (a.prob_local) a.prob_local[i - a.row0] = 1.f / ss;  // e^{m - lse}
   }
-  if (chunk_id == 0 && threadIdx.x == 0) {
+  if (chunk_id == 0 && threadIdx.x == kRowWriter) {  // not a thread that pushed to peers
     a.lse[i] = l;
     a.row_loss_all[i] = l - zz;
     if (a.row_loss_local && i >= a.row0 && i < a.row0 + a.B) a.row_loss_local[i - a.row0] = l - zz;
   }
+  // ---- mean loss (chunk-0 CTAs, before their G chunk so the ticket's fence covers only the
+  //      row-loss stores): the last one sums all rows in a fixed order
+  if (chunk_id == 0) mean_loss_ticket(a);
   // ---- G for this CTA's chunk of the row
+  const bool tl = g_trace_on && threadIdx.x == 0 && i == a.Bt - 1 && chunk_id == static_cast<int>(gridDim.y) - 1;
+  if (tl) g_dbg_ts[21] = gtime_ns();
   grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, chunk_id, mt, l, yl);
-  if (chunk_id != 0 || !last_of_n(a.counter, gridDim.x)) return;  // loss: chunk-0 CTAs only
-  double acc = 0.0;
-  for (int r = threadIdx.x; r < a.Bt; r += kStatsThreads) acc += static_cast<double>(__ldcg(a.row_loss_all + r));
-  __shared__ double part[4];
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *a.loss = static_cast<float>(((part[0] + part[1]) + (part[2] + part[3])) / a.Bt);
-    *a.counter = 0;
-  }
+  if (tslot >= 0) g_dbg_ts[tslot + 4] = gtime_ns();
+  if (tl) g_dbg_ts[22] = gtime_ns();
 }
 
 // ---------------------------------------------------------------- A8 dX reduce-scatter (owner)

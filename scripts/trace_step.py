@@ -50,8 +50,9 @@ for it in range(int(os.environ.get("ITERS", "5"))):
     rec = {names[k]: [round((buf[2 * k] - t0) / 1e3, 1), round((buf[2 * k + 1] - t0) / 1e3, 1)]
            for k in range(len(names)) if buf[2 * k + 1]}
     tend = max(v[1] for v in rec.values())
-    stamps = {"row0": [round((st[16 + j] - t0) / 1e3, 1) for j in range(4) if st[16 + j] >= t0],
-              "rowLast": [round((st[24 + j] - t0) / 1e3, 1) for j in range(4) if st[24 + j] >= t0]}
+    stamps = {"row0": [round((st[16 + j] - t0) / 1e3, 1) for j in range(5) if st[16 + j] >= t0],
+              "rowLast": [round((st[24 + j] - t0) / 1e3, 1) for j in range(5) if st[24 + j] >= t0],
+              "rowLast_lastchunk": [round((st[21 + j] - t0) / 1e3, 1) for j in range(2) if st[21 + j] >= t0]}
     out.append({"rank": rank, "it": it, "span_us": tend, "win_us": rec, "stats_stamps": stamps})
 L.whale_debug_trace_enable(0)
 op.check()
