@@ -128,6 +128,22 @@ def host_cores():
     return len(os.sched_getaffinity(0))
 
 
+_BLAS_LIMIT = None
+
+
+def oracle_threads() -> int:
+    """Let the oracle's BLAS use every host core (torchrun exports OMP_NUM_THREADS=1 to its
+    workers) and return the thread count it actually runs with."""
+    global _BLAS_LIMIT
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        _BLAS_LIMIT = threadpool_limits(limits=host_cores(), user_api="blas")
+        n = [p.get("num_threads", 1) for p in threadpool_info() if p.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return int(os.environ.get("OMP_NUM_THREADS", host_cores()))
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -311,8 +327,9 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
+        threads = oracle_threads()
         sps, n, el = time_oracle(cfg, seed, args.cpu_seconds, rows=min(cfg.B * world, 64))
-        cpu = {"value": sps, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+        cpu = {"value": sps, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"{n} x fp64 numpy fwd+bwd of {min(cfg.B * world, 64)} rows of {args.config} "
                          f"(D={cfg.D}, C={cfg.C}) in {el:.1f} s"}
 
@@ -427,6 +444,7 @@ def run_reference(args, cfg, seed, world, rank):
     if rank != 0:
         return
     rows = min(cfg.B * world, 32)  # same sample as the cpu_baseline leg
+    threads = oracle_threads()
     import oracle
     X = syn.gen_features((0, rows), cfg.D, seed, cfg.dtype).double().numpy()
     y = syn.gen_labels((0, rows), cfg.C, seed).numpy()
@@ -444,7 +462,7 @@ def run_reference(args, cfg, seed, world, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded)",
         "config": {"workload": workload_desc(args.config, cfg, world), "D": cfg.D, "C": cfg.C,
                    "B_per_gpu": cfg.B, "global_batch": cfg.B * world},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                          "sample": f"each step: fp64 numpy fwd+bwd of {rows} rows of {args.config} (D={cfg.D}, C={cfg.C})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
