@@ -374,8 +374,9 @@ def kernel_work(name, cfgj, cfg, es):
     if f1 and name == "logits_gemm":  # F1: read W_r once, X; write P~, tile stats, U partials
         return (Cr * D * es + Bt * D * es + Bt * Cr * es + 3 * Bt * T * 4 + ncl * Bt * D * 4 + ncl * Bt * 4,
                 4 * Bt * Cr * D)
-    if f1 and name == "bwd_gemm":     # F1: dW tiles only
-        return kernel_work("dw_gemm", cfgj, cfg, es)
+    if f1 and name == "bwd_gemm":     # F1: dW tiles + the dX combine units (U partials -> dX)
+        bw, fw = kernel_work("dw_gemm", cfgj, cfg, es)
+        return bw + ncl * Bt * D * 4 + Bt * D * es + Bt * D * (es if world == 1 else 4), fw
     if f1 and name == "dx_gemm":      # F1 combine: read U partials + label rows of W, write dX
         return ncl * Bt * D * 4 + Bt * D * es + Bt * D * (es if world == 1 else 4), 0
     if name == "logits_gemm":   # read W_r, X; write P~ and tile stats

@@ -20,13 +20,106 @@
 
 namespace whale {
 
+// F1 dX combine as work units of the backward kernel (scheduled first, while U is L2-resident;
+// the dynamic scheduler balances the dW tiles around them):
+// unit (row b, 1024-column part) computes dX[b, part] = (1/B_tot)(sum_cl e^{uref - lse} U_cl -
+// W_{y_b}) in fixed cluster order; N = 1 writes dX, N > 1 pushes to the row owner's slab.
+struct CombineArgs {
+  const float* upart;   // [ncl x B_tot x D]
+  const float* uref;    // [ncl x B_tot]
+  int ncl, Bt, D, parts;
+  const float* lse;     // [B_tot]
+  const int32_t* y;     // [B_tot] global labels
+  long long o_r, C_r;
+  const void* w;        // W_r bf16 [C_r x D]
+  float inv_bt;
+  void* dx_out;         // N = 1: dX bf16 [B_tot x D]
+  PeerPtrs recv;        // N > 1: owners' fp32 slabs [world][B_max x D]
+  int row_off[kMaxRanks + 1];
+  int rank, world, Bslab;
+};
+
 struct BwdArgs {
   GemmArgs dx;          // units [0, ux): M = B_tot, N = D, K = C_r (A = G K-major, B = W_r MN-major)
   GemmArgs dw;          // units [ux, ux + tw): M = C_r, N = D, K = B_tot (both MN-major)
   int ux, tw;
+  int tc;               // F1 dX combine units (no TMEM / smem stages), scheduled FIRST: unit ids
+                        // [0, tc) are combine units and the GEMM units above are shifted by tc
+  CombineArgs cb;
   int stages, stage_bytes, epi_bufs;  // epi_bufs: CTA-wide 16 KB store stages
-  unsigned* sched_cnt;  // monotonic dynamic-scheduler counter: (e - 1) * (ux + tw) at launch
+  unsigned* sched_cnt;  // monotonic dynamic-scheduler counter: (e - 1) * (ux + tw + tc) at launch
 };
+
+constexpr int kCombineCols = 1024;  // dX columns per combine unit (128 threads x 2 float4)
+
+// One combine unit, by the 128 epilogue threads (named barrier 1); fac: >= ncl floats of smem.
+__device__ __forceinline__ void combine_unit(const CombineArgs& c, int u, float* fac) {
+  const int b = u / c.parts, part = u % c.parts;
+  const int et = threadIdx.x - 128;
+  const float l = c.lse[b];
+  for (int i = et; i < c.ncl; i += 128) fac[i] = __expf(c.uref[static_cast<size_t>(i) * c.Bt + b] - l);
+  named_bar_sync(1, 128);
+  const long long lab = static_cast<long long>(c.y[b]) - c.o_r;
+  const bool own = lab >= 0 && lab < c.C_r;
+  const size_t cstride = static_cast<size_t>(c.Bt) * c.D;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int d = part * kCombineCols + (h * 128 + et) * 4;
+    if (d >= c.D) continue;
+    const float* src = c.upart + static_cast<size_t>(b) * c.D + d;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int i = 0;
+    for (; i + 4 <= c.ncl; i += 4) {  // four independent loads in flight, fixed summation order
+      float4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __ldcg(reinterpret_cast<const float4*>(src + (i + k) * cstride));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float f = fac[i + k];
+        acc.x = fmaf(f, v[k].x, acc.x);
+        acc.y = fmaf(f, v[k].y, acc.y);
+        acc.z = fmaf(f, v[k].z, acc.z);
+        acc.w = fmaf(f, v[k].w, acc.w);
+      }
+    }
+    for (; i < c.ncl; ++i) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(src + i * cstride));
+      const float f = fac[i];
+      acc.x = fmaf(f, v.x, acc.x);
+      acc.y = fmaf(f, v.y, acc.y);
+      acc.z = fmaf(f, v.z, acc.z);
+      acc.w = fmaf(f, v.w, acc.w);
+    }
+    if (own) {  // the one-hot term, on the shard that owns the label
+      const uint2 raw = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(c.w) + lab * c.D + d);
+      const float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+      const float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+      acc.x -= w01.x;
+      acc.y -= w01.y;
+      acc.z -= w23.x;
+      acc.w -= w23.y;
+    }
+    acc.x *= c.inv_bt;
+    acc.y *= c.inv_bt;
+    acc.z *= c.inv_bt;
+    acc.w *= c.inv_bt;
+    if (c.world == 1) {
+      uint2 o;
+      o.x = pack_bf16x2(acc.x, acc.y);
+      o.y = pack_bf16x2(acc.z, acc.w);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(c.dx_out) + static_cast<size_t>(b) * c.D + d) = o;
+    } else {
+      int owner = 0;
+#pragma unroll
+      for (int r = 1; r < kMaxRanks; ++r)
+        if (r < c.world && c.row_off[r] <= b) owner = r;
+      float* dst = reinterpret_cast<float*>(c.recv.p[owner]) +
+                   (static_cast<size_t>(c.rank) * c.Bslab + (b - c.row_off[owner])) * c.D + d;
+      *reinterpret_cast<float4*>(dst) = acc;  // NVLink store into the owner's slab
+    }
+  }
+  named_bar_sync(1, 128);  // fac is reused by the next unit
+}
 
 constexpr int kSchedSlots = 4;
 
@@ -39,6 +132,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ int s_fix_go;
   __shared__ int sched_tile[kSchedSlots];
+  __shared__ float s_fac[160];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* epi_smem = smem + a.stages * a.stage_bytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + a.epi_bufs * 4 * kEpiBufBytes);
@@ -54,7 +148,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int kKStepMN = (32 / ES) * kRowBytes;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int total = a.ux + a.tw;
+  const int total = a.ux + a.tw + a.tc;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
@@ -111,6 +205,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         sched_tile[slot] = unit;
         mbar_arrive(&sfull[slot]);
         if (unit < 0) break;
+        if (unit < a.tc) continue;  // combine unit: epilogue-only work
+        unit -= a.tc;
         int mb, nb, sp, kb0, kb1;
         if (unit < a.ux) {
           decode_tile(X, unit, mb, nb, sp, kb0, kb1);
@@ -157,18 +253,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int dw_kmma = a.dw.bk / (32 / ES);
       int stage = 0;
       uint32_t phase = 0;
+      int na = 0;  // GEMM units so far (accumulator ring index; combine units use no TMEM)
       for (int it = 0;; ++it) {
         const int slot = it % kSchedSlots;
         mbar_wait(&sfull[slot], (it / kSchedSlots) & 1);
         const int unit = sched_tile[slot];
         mbar_arrive(&sempty[slot]);
         if (unit < 0) break;
-        const bool is_dx = unit < a.ux;
+        if (unit < a.tc) continue;
+        const int gu = unit - a.tc;
+        const bool is_dx = gu < a.ux;
         int mb, nb, sp, kb0, kb1;
-        if (is_dx) decode_tile(a.dx, unit, mb, nb, sp, kb0, kb1);
-        else decode_tile(a.dw, unit - a.ux, mb, nb, sp, kb0, kb1);
-        const int acc = it & 1;
-        const uint32_t aph = (it >> 1) & 1;
+        if (is_dx) decode_tile(a.dx, gu, mb, nb, sp, kb0, kb1);
+        else decode_tile(a.dw, gu - a.ux, mb, nb, sp, kb0, kb1);
+        const int acc = na & 1;
+        const uint32_t aph = (na >> 1) & 1;
+        ++na;
         mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kMaxBN;
@@ -206,6 +306,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;
     const int nbuf = a.epi_bufs;
     int buf = 0;
+    int na = 0;  // GEMM units so far (accumulator ring index)
     for (int it = 0;; ++it) {
       const int slot = it % kSchedSlots;
       mbar_wait(&sfull[slot], (it / kSchedSlots) & 1);
@@ -213,13 +314,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&sempty[slot]);
       if (unit < 0) break;
-      const bool is_dx = unit < a.ux;
+      if (unit < a.tc) {
+        combine_unit(a.cb, unit, s_fac);
+        continue;
+      }
+      const int gu = unit - a.tc;
+      const bool is_dx = gu < a.ux;
       const GemmArgs& g = is_dx ? a.dx : a.dw;
       int mb, nb, sp, kb0, kb1;
-      decode_tile(g, is_dx ? unit : unit - a.ux, mb, nb, sp, kb0, kb1);
+      decode_tile(g, is_dx ? gu : gu - a.ux, mb, nb, sp, kb0, kb1);
       const CUtensorMap* om = is_dx ? &tmPart : &tmDW;
-      const int acc = it & 1;
-      const uint32_t aph = (it >> 1) & 1;
+      const int acc = na & 1;
+      const uint32_t aph = (na >> 1) & 1;
+      ++na;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * kMaxBN + (static_cast<uint32_t>(q * 32) << 16);

@@ -689,7 +689,9 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     c->bwd_stage_bytes = p.f1 ? p.dw.stage_bytes : std::max(p.dx.stage_bytes, p.dw.stage_bytes);
     c->bwd_epi_bufs = env_int("WHALE_BWD_EPI", p.f1 ? 8 : 4);  // CTA-wide 16 KB store stages (dW-only: deeper)
     const int fixed = 1024 + 512 + c->bwd_epi_bufs * 4 * kEpiBufBytes;
-    c->bwd_stages = std::min(8, (kSmemLimit - kStaticSmemSlack - fixed) / c->bwd_stage_bytes);
+    cudaFuncAttributes fa{};
+    CUDA_TRY(cudaFuncGetAttributes(&fa, splitfc_bwd_kernel<2>));  // the kernel's own __shared__ bytes
+    c->bwd_stages = std::min(8, (kSmemLimit - static_cast<int>(fa.sharedSizeBytes) - fixed) / c->bwd_stage_bytes);
     c->bwd_smem = fixed + c->bwd_stages * c->bwd_stage_bytes;
     if (c->bwd_stages < 2) c->fused_bwd = false;
   }
@@ -1065,8 +1067,9 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       ax.rs_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_RS * kMaxRanks + p.rank;
     }
   }
-  if (ES == 2 && p.f1) {
+  if (ES == 2 && p.f1 && !c->fused_bwd) {
     // ---- A8 from the forward's U partials: dX = (1/B_tot)(sum_cl e^{ref - lse} U_cl - W_y)
+    //      (with the fused backward these are work units of the backward kernel instead)
     RowSplit rs{};
     PeerPtrs recv{};
     for (int r = 0; r <= p.world; ++r) rs.off[r] = static_cast<int>(p.Boff[r]);
@@ -1094,11 +1097,34 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     b.dw.err = err;
     b.ux = p.f1 ? 0 : p.dx.num_tiles;
     b.tw = p.dw.num_tiles;
+    if (p.f1) {  // F1: dX = (1/B_tot)(sum_cl e^{ref - lse} U_cl - W_y) as the schedule's last units
+      CombineArgs& cb = b.cb;
+      cb.upart = wsp<float>(c, L.upart);
+      cb.uref = wsp<float>(c, L.uref);
+      cb.ncl = p.f1_ncl;
+      cb.Bt = static_cast<int>(p.Bt);
+      cb.D = static_cast<int>(p.D);
+      cb.parts = cdiv(p.D, kCombineCols);
+      cb.lse = wsp<float>(c, L.lse);
+      cb.y = yg;
+      cb.o_r = p.o_r;
+      cb.C_r = p.Cr;
+      cb.w = w;
+      cb.inv_bt = static_cast<float>(1.0 / static_cast<double>(p.Bt));
+      cb.dx_out = dx_local;
+      for (int r = 0; r <= p.world; ++r) cb.row_off[r] = static_cast<int>(p.Boff[r]);
+      if (p.world > 1)
+        for (int r = 0; r < p.world; ++r) cb.recv.p[r] = c->symm[r] + L.dxrecv;
+      cb.rank = p.rank;
+      cb.world = p.world;
+      cb.Bslab = static_cast<int>(p.Bmax);
+      b.tc = static_cast<int>(p.Bt) * cb.parts;
+    }
     b.stages = c->bwd_stages;
     b.stage_bytes = c->bwd_stage_bytes;
     b.epi_bufs = c->bwd_epi_bufs;
     b.sched_cnt = counters + CNT_SCHED;
-    const int grid = std::min(b.ux + b.tw, p.sms);
+    const int grid = std::min(b.ux + b.tw + b.tc, p.sms);
     auto kern = splitfc_bwd_kernel<2>;
     static bool attr = false;
     if (!attr) {
@@ -1195,7 +1221,8 @@ extern "C" int32_t whale_splitfc_launches_per_step(const whale_splitfc_ctx* ctx)
   if (!ctx) return 0;
   // N = 1: logits, stats+grad, dW, dX;  N > 1: + gather, + dX owner reduce
   int base = ctx->p.world == 1 ? 4 : 6;
-  if (ctx->fused_bwd) base -= 1;  // dW + dX share one launch
+  if (ctx->fused_bwd) base -= 1;  // dW + dX share one launch (F1: dW tiles + dX combine units)
+  else if (ctx->p.f1) base += 0;    // F1 unfused: the dX GEMM is replaced by the combine kernel
   return base + (ctx->p.es == 4 ? 3 : 0);  // fp32 path: operand transposes
 }
 

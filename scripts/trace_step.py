@@ -41,7 +41,10 @@ for it in range(int(os.environ.get("ITERS", "5"))):
     if group is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    g.replay()
+    if os.environ.get("NOGRAPH"):
+        step()
+    else:
+        g.replay()
     buf = (ctypes.c_ulonglong * 32)()
     L.whale_debug_trace_read(buf)
     st = (ctypes.c_ulonglong * 32)()
