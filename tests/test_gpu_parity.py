@@ -290,3 +290,40 @@ def test_bias_and_predictions(whale, B, D, C, dtype):
     assert np.array_equal(pred[clear], f["pred"][clear])
     assert np.all((pred >= 0) & (pred < C))
     np.testing.assert_allclose(prob, f["prob"], rtol=5e-3 if dtype == "f32" else 1e-3)
+
+
+@pytest.mark.parametrize("B,D,C", [(32, 2048, 20_000), (64, 512, 5000)])
+def test_cuda_graph_replay(whale, B, D, C):
+    """The bench captures one step as a CUDA graph and replays it: the device-resident step
+    epoch must make every replay compute the same thing as an eager step (F1 and plain path)."""
+    seed = 400 + B
+    X = syn.gen_features((0, B), D, seed, "bf16").cuda()
+    W = syn.gen_weight((0, C), D, seed, "peaked", "bf16").cuda()
+    y = syn.gen_labels((0, B), C, seed).cuda().to(torch.int32)
+    op = whale.SplitFCSoftmaxCE(C, D, B)
+    dx = torch.empty(B, D, dtype=torch.bfloat16, device="cuda")
+    dw = torch.empty(C, D, dtype=torch.float32, device="cuda")
+    op.forward(X, y, W)
+    op.backward(W, dx, dw)
+    torch.cuda.synchronize()
+    ref = (op.loss.clone(), dx.clone(), dw.clone())
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        op.forward(X, y, W)  # warm-up on the capture stream
+        op.backward(W, dx, dw)
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        op.forward(X, y, W)
+        op.backward(W, dx, dw)
+    for _ in range(3):
+        dx.zero_()
+        dw.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        op.check()
+        assert torch.equal(op.loss, ref[0])
+        assert torch.equal(dx, ref[1])
+        assert torch.equal(dw, ref[2])
+    op.close()
