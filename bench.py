@@ -46,8 +46,18 @@ def load_peaks():
         return dict(FALLBACK_PEAKS)
 
 
+def capacity_for(cfg, world):
+    """The config's capacity weights for `world` ranks (c3's 2:1:...:1 pattern keeps its first
+    `world` entries, so the uneven plan also runs on fewer than 8 GPUs)."""
+    if cfg.capacity is None:
+        return None
+    cap = list(cfg.capacity[:world]) + [1] * max(0, world - len(cfg.capacity))
+    return cap if world > 1 else None
+
+
 def workload_desc(name, cfg, world):
-    shards = "even" if cfg.capacity is None else ":".join(str(c) for c in cfg.capacity)
+    cap = capacity_for(cfg, world)
+    shards = "even" if cap is None else ":".join(str(c) for c in cap)
     return (f"{name}: D={cfg.D}, C={cfg.C}, B={cfg.B}/GPU x {world} GPU(s), {cfg.dtype}, {shards} class shards "
             f"(split-FC softmax-CE, Whale hybrid DP+MP)")
 
@@ -183,7 +193,8 @@ def main():
     _lib.lib()
 
     dtype = syn.torch_dtype(cfg.dtype)
-    op = whale.SplitFCSoftmaxCE(cfg.C, cfg.D, cfg.B, capacity=cfg.capacity, dtype=dtype, group=group, device=dev)
+    op = whale.SplitFCSoftmaxCE(cfg.C, cfg.D, cfg.B, capacity=capacity_for(cfg, world), dtype=dtype, group=group,
+                                device=dev)
     C_r, o_r = op.C_r, op.o_r
     X = syn.gen_features((rank * cfg.B, (rank + 1) * cfg.B), cfg.D, seed, cfg.dtype, device=dev)
     y = syn.gen_labels((rank * cfg.B, (rank + 1) * cfg.B), cfg.C, seed, device=dev).to(torch.int32)
