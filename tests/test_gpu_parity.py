@@ -184,8 +184,9 @@ def test_deterministic_bitwise(whale):
     assert torch.equal(res[0][2], res[1][2])
 
 
-def test_label_out_of_range_detected(whale):
-    B, D, C = 8, 64, 100
+@pytest.mark.parametrize("D", [64, 512])  # plain path and F1
+def test_label_out_of_range_detected(whale, D):
+    B, C = 8, 100
     X = syn.gen_features((0, B), D, 11, "bf16").cuda()
     W = syn.gen_weight((0, C), D, 11, "init", "bf16").cuda()
     y = torch.tensor([0, 1, 2, 100, 4, 5, 6, 7], dtype=torch.int32, device="cuda")
