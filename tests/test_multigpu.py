@@ -1,4 +1,4 @@
-"""Multi-GPU parity (N = 2 / 4 / 8 on one box): launches scripts/mgpu_parity.py under
+"""Multi-GPU parity (N = 2 / 4 / 8 on one box): launches tests/mgpu_parity_worker.py under
 torchrun with one rank per visible GPU; each rank checks its dX_r rows and dW_r shard
 against the unsharded fp64 oracle and the loss must be bit-identical on all ranks
 (even, uneven 2:1:..., fp32 and the c2 shape).  Skipped with fewer than 2 GPUs."""
@@ -26,7 +26,7 @@ def _port():
 def test_multigpu_parity():
     n = min(torch.cuda.device_count(), 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(n), "--master-addr",
-           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "scripts", "mgpu_parity.py")]
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", "mgpu_parity_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert '"ok": false' not in r.stdout
