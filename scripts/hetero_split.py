@@ -17,8 +17,11 @@ rank, world = dist.get_rank(), dist.get_world_size()
 local = int(os.environ["LOCAL_RANK"]); torch.cuda.set_device(local); dev = torch.device("cuda", local)
 cfg = syn.CONFIGS["c2"]
 res = []
-plans = [("even", None, None), ("proportional 2:1", [2] + [1] * (world - 1), None),
-         ("alg1 2:1, rank0 capped at 55% of C", [2] + [1] * (world - 1),
+# HETERO_CAP="2,2,1,1": capacity weights of the proportional plan (default 2:1:...:1)
+capw = [int(v) for v in os.environ.get("HETERO_CAP", ",".join(["2"] + ["1"] * (world - 1))).split(",")]
+tag = ":".join(str(v) for v in capw)
+plans = [("even", None, None), (f"proportional {tag}", capw, None),
+         (f"alg1 {tag}, rank0 capped at 55% of C", capw,
           [int(0.55 * cfg.C * cfg.D * 6)] + [10 ** 12] * (world - 1))]
 for name, cap, mem in plans:
     op = SplitFCSoftmaxCE(cfg.C, cfg.D, cfg.B, capacity=cap, group=dist.group.WORLD, device=dev, mem_bytes=mem)
@@ -45,5 +48,6 @@ for name, cap, mem in plans:
     del op
 if rank == 0:
     for r in res:
-        print(json.dumps({"sm_limit_r1": os.environ.get("WHALE_SM_LIMIT_R1"), **r}))
+        caps = {k: v for k, v in os.environ.items() if k.startswith("WHALE_SM_LIMIT_R")}
+        print(json.dumps({"world": world, "sm_limits": caps, **r}))
 dist.barrier(); dist.destroy_process_group()
