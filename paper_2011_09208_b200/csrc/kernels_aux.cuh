@@ -296,10 +296,13 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
       if (a.prob_local) a.prob_local[i] = 1.f / s;  // e^{m - lse}
     }
   }
-  // ---- mean loss (chunk-0 CTAs, before their G chunk): the last one sums all rows in order
-  if (blockIdx.x == 0) mean_loss_ticket(a);
-  // ---- G for this CTA's chunk of the row
-  grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, blockIdx.x, mt, l, yl);
+  // ---- block 0 of a row: the row's results and the mean-loss ticket only; blocks >= 1
+  //      rewrite G chunk blockIdx.x - 1 (keeps the ticket's fence off the rewrite path)
+  if (blockIdx.x == 0) {
+    mean_loss_ticket(a);
+    return;
+  }
+  grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, blockIdx.x - 1, mt, l, yl);
 }
 
 // ---------------------------------------------------------------- A4-A6 fused (N > 1)
@@ -409,7 +412,8 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
   // ---- G for this CTA's chunk of the row
   const bool tl = g_trace_on && threadIdx.x == 0 && i == a.Bt - 1 && chunk_id == static_cast<int>(gridDim.y) - 1;
   if (tl) g_dbg_ts[21] = gtime_ns();
-  grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, chunk_id, mt, l, yl);
+  if (chunk_id == 0) return;  // the row's stats / exchange CTA rewrites no G chunk
+  grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, chunk_id - 1, mt, l, yl);
   if (tslot >= 0) g_dbg_ts[tslot + 4] = gtime_ns();
   if (tl) g_dbg_ts[22] = gtime_ns();
 }

@@ -961,7 +961,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     if (p.world == 1) {
       // A4-A6 fused: lse, loss and G in one pass (no exchange needed)
       PROFILED(K_STATS, s,
-               (launch(c, stats_grad_kernel<ES>, dim3(cdiv(p.Cr, chunk), p.Bt), dim3(kStatsThreads), 0, s, a,
+               (launch(c, stats_grad_kernel<ES>, dim3(cdiv(p.Cr, chunk) + 1, p.Bt), dim3(kStatsThreads), 0, s, a,
                        static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
                        static_cast<float>(1.0 / static_cast<double>(p.Bt)))));
     } else {
@@ -970,7 +970,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
       for (int r = 0; r < p.world; ++r)
         rf.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.rowflags) + static_cast<size_t>(p.rank) * p.Bt;
       PROFILED(K_STATS, s,
-               (launch(c, stats_grad_multi_kernel<ES>, dim3(p.Bt, cdiv(p.Cr, chunk)), dim3(kStatsThreads), 0, s, a,
+               (launch(c, stats_grad_multi_kernel<ES>, dim3(p.Bt, cdiv(p.Cr, chunk) + 1), dim3(kStatsThreads), 0, s, a,
                        static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
                        static_cast<float>(1.0 / static_cast<double>(p.Bt)), rf,
                        reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.rowflags))));
