@@ -559,19 +559,33 @@ static whale_status_t launch(whale_splitfc_ctx* c, void (*kern)(KArgs...), dim3 
   return WHALE_OK;
 }
 
-static bool g_attr_done[8] = {};
+// cudaFuncSetAttribute acts on the current device: remember per (device, kernel slot) that the
+// opt-in shared-memory limit has been raised (slots 0..7: GEMMs, 8: fused backward).
+static constexpr int kMaxDevices = 64;
+static bool g_attr_done[kMaxDevices][9] = {};
+
+template <typename K>
+static whale_status_t ensure_smem_attr(K kern, int slot) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= kMaxDevices) return fail(WHALE_ERR_UNSUPPORTED, "device index %d", dev);
+  if (g_attr_done[dev][slot]) return WHALE_OK;
+  cudaFuncAttributes fa{};
+  CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
+  g_attr_done[dev][slot] = true;
+  return WHALE_OK;
+}
 
 template <int EPI, bool AMN, bool BMN, int ES>
 static whale_status_t launch_gemm(whale_splitfc_ctx* c, int slot, const GemmCfg& g, const CUtensorMap& A,
                                   const CUtensorMap& B, const CUtensorMap& O, const GemmArgs& args,
                                   cudaStream_t s) {
   auto kern = splitfc_gemm_kernel<EPI, AMN, BMN, ES>;
-  if (!g_attr_done[slot]) {
-    cudaFuncAttributes fa{};
-    CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
-    g_attr_done[slot] = true;
+  {
+    const whale_status_t st = ensure_smem_attr(kern, slot);
+    if (st != WHALE_OK) return st;
   }
   if (g.cluster <= 1) return launch(c, kern, dim3(g.grid), dim3(kGemmThreads), g.smem, s, A, B, O, args);
   cudaLaunchConfig_t cfg{};
@@ -1126,13 +1140,9 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     b.sched_cnt = counters + CNT_SCHED;
     const int grid = std::min(b.ux + b.tw + b.tc, p.sms);
     auto kern = splitfc_bwd_kernel<2>;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncAttributes fa{};
-      CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
-      CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
-      attr = true;
+    {
+      const whale_status_t st = ensure_smem_attr(kern, 8);
+      if (st != WHALE_OK) return st;
     }
     PROFILED(K_BWD, s,
              (launch(c, kern, dim3(grid), dim3(kGemmThreads), c->bwd_smem, s, c->tmG_dx, c->tmW_dx, c->tmDxPart,
