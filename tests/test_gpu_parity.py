@@ -330,3 +330,40 @@ def test_cuda_graph_replay(whale, B, D, C):
         assert torch.equal(dx, ref[1])
         assert torch.equal(dw, ref[2])
     op.close()
+
+
+def test_random_shapes_fuzz(whale):
+    """Seeded random shapes across both paths (F1 when B_tot <= 32 and D % 256 == 0, else the
+    plain GEMMs): loss / dX / dW / db / predictions against the oracle."""
+    rng = np.random.default_rng(2011_09208)
+    for case in range(24):
+        f1 = case % 2 == 0
+        B = int(rng.integers(1, 33)) if f1 else int(rng.integers(1, 300))
+        D = int(rng.choice([256, 512, 768, 1024, 1536, 2048])) if f1 else int(rng.integers(1, 96)) * 8
+        C = int(rng.integers(1, 9000))
+        regime = str(rng.choice(["init", "peaked"]))
+        bias = bool(rng.integers(0, 2))
+        seed = 500 + case
+        X = syn.gen_features((0, B), D, seed, "bf16")
+        W = syn.gen_weight((0, C), D, seed, regime, "bf16")
+        y = syn.gen_labels((0, B), C, seed)
+        b = syn.gen_bias((0, C), seed, 1.0, "bf16") if bias else None
+        op = whale.SplitFCSoftmaxCE(C, D, B)
+        xd, wd = X.cuda(), W.cuda()
+        bd = b.cuda() if bias else None
+        loss = float(op.forward(xd, y.cuda(), wd, row_loss=True, bias=bd, predictions=True))
+        out = op.backward(wd, bias_grad=bias)
+        op.check()
+        f = oracle.forward_backward(X, W, y.numpy(), b)
+        tag = f"case {case}: B={B} D={D} C={C} {regime} bias={bias} f1={op.config()['f1']}"
+        assert abs(loss - f["loss"]) <= LOSS_RTOL * max(abs(f["loss"]), 1e-3), tag
+        if np.linalg.norm(f["dX"]) > 0:
+            assert _fro(out[0].float().cpu(), f["dX"]) <= FRO_RTOL, tag
+        if np.linalg.norm(f["dW"]) > 0:
+            assert _fro(out[1].cpu(), f["dW"]) <= FRO_RTOL, tag
+        if bias and np.linalg.norm(f["db"]) > 0:
+            assert _fro(out[2].cpu(), f["db"]) <= FRO_RTOL, tag
+        Z = np.sort(f["Z"], axis=1)
+        clear = (Z[:, -1] - Z[:, -2]) > 1e-3 if C > 1 else np.ones(B, bool)
+        assert np.array_equal(op.pred.cpu().numpy()[clear], f["pred"][clear]), tag
+        op.close()
