@@ -6,7 +6,9 @@ What runs here without a GPU:
 * the exchange protocol of the CUDA path, restated on the host with gloo collectives:
   per-shard statistics (m_r, s_r, z_y,r) -> all-gather of the records -> rank-ordered
   combine -> loss identical on every rank; the reduce-scatter of dX partials by row owner
-  (row // B) -- checked against the unsharded fp64 oracle.
+  (row // B) -- checked against the unsharded fp64 oracle;
+* NEXT-3 uneven per-rank batches: descriptor sizes agree, gather-v by padding, row owners from
+  the prefix offsets, the dX reduce-scatter against the oracle.
 The GPU kernels implement the same protocol over NVLink (tests/test_multigpu.py).
 """
 import os
@@ -96,6 +98,37 @@ def _worker(rank, world, port, q):
         out["loss_ok"] = abs(loss - f["loss"]) <= 1e-12 * abs(f["loss"])
         out["dW_ok"] = np.allclose(dW_r, f["dW"][o:o + c], rtol=1e-10, atol=1e-15)
         out["dX_ok"] = np.allclose(dX_r, f["dX"][rank * B:(rank + 1) * B], rtol=1e-10, atol=1e-15)
+        # ---- NEXT-3: uneven per-rank batch (proportional split of the global batch)
+        bc, _ = _lib.whale_splitfc_plan(7, world, [2, 1])    # [5, 2]
+        offs_b = np.concatenate([[0], np.cumsum(bc)])
+        d2, _k2 = _lib.make_desc(rank, world, bc[rank], D, C, counts, offs, batch_counts=bc)
+        symm2, _ = _lib.whale_splitfc_workspace_size(d2)
+        alls2 = [None] * world
+        dist.all_gather_object(alls2, symm2)
+        out["uneven_symm_equal"] = all(v == alls2[0] for v in alls2)
+        Bt2 = int(offs_b[-1])
+        X2 = np.maximum(rng.standard_normal((Bt2, D)), 0)
+        y2 = rng.integers(0, C, Bt2)
+        mine = torch.from_numpy(X2[offs_b[rank]:offs_b[rank + 1]].copy())
+        bmax = int(max(bc))
+        padded = torch.zeros(bmax, D, dtype=torch.float64)
+        padded[:bc[rank]] = mine
+        xs2 = [torch.zeros(bmax, D, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(xs2, padded)                         # gather-v via padding to B_max
+        Xg2 = torch.cat([xs2[p][:bc[p]] for p in range(world)]).numpy()
+        out["uneven_gather_ok"] = np.array_equal(Xg2, X2)
+        # each shard's dX partial, reduce-scattered to the row owner found from the prefix offsets
+        f2 = oracle.forward_backward(X2, W, y2)
+        G2 = f2["G"][:, o:o + c]
+        part2 = G2 @ W[o:o + c]
+        owner = np.searchsorted(offs_b, np.arange(Bt2), side="right") - 1
+        mine_rows = np.nonzero(owner == rank)[0]
+        send = [torch.from_numpy(np.ascontiguousarray(part2[owner == p])) for p in range(world)]
+        recv = [[torch.zeros(int(bc[p]), D, dtype=torch.float64) for _ in range(world)] for p in range(world)]
+        for p in range(world):
+            dist.all_gather(recv[p], send[p])
+        dX2 = sum(recv[rank][src] for src in range(world)).numpy()
+        out["uneven_dX_ok"] = np.allclose(dX2, f2["dX"][mine_rows], rtol=1e-10, atol=1e-15)
         q.put((rank, out))
     except Exception as e:  # report instead of hanging the parent
         q.put((rank, {"error": repr(e)}))
