@@ -154,6 +154,9 @@ whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, whale_splitf
  *   x_local  [B x D] device; labels_local [B] int32 device; w_shard [C_r x D] device
  *   loss     device float scalar (identical bits on every rank)
  *   row_loss device [B] per-row loss of this rank's rows, or NULL
+ * With bf16 operands, B_tot <= 32 and D % 256 == 0, D <= 2048 the forward also accumulates
+ * the dX partials U = sum_t P~_t W_t (one pass over W_r) and the backward only
+ * finishes them -- same results, W_r read once per step.
  * Saves y, P~ and the statistics in the workspace for the following backward; X is saved
  * there too when world_size > 1 (the gathered batch).  At world_size 1 X is NOT copied: the
  * backward reads x_local itself, so it must stay valid and unmodified until the matching
