@@ -367,3 +367,18 @@ def test_random_shapes_fuzz(whale):
         clear = (Z[:, -1] - Z[:, -2]) > 1e-3 if C > 1 else np.ones(B, bool)
         assert np.array_equal(op.pred.cpu().numpy()[clear], f["pred"][clear]), tag
         op.close()
+
+
+def test_f1_reference_moves(whale):
+    """F1's lazy per-row reference must move (U rescaled in TMEM) when later class tiles hold
+    much larger logits: scale W's rows up along the class index so every cluster's later tiles
+    exceed its first tile's max by far more than the 2^8 threshold."""
+    B, D, C = 32, 512, 40_000
+    X = syn.gen_features((0, B), D, 77, "bf16")
+    W0 = syn.gen_weight((0, C), D, 77, "peaked", "bf16").float()
+    ramp = torch.linspace(0.2, 3.0, C).unsqueeze(1)
+    W = (W0 * ramp).to(torch.bfloat16)
+    y = syn.gen_labels((0, B), C, 77)
+    g = _run(whale, X, W, y)
+    assert g["cfg"]["f1"] == 1
+    _check_full(g, oracle.forward_backward(X, W, y.numpy()), "f1 reference moves")
