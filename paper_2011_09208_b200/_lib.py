@@ -118,6 +118,8 @@ def whale_splitfc_plan(num_classes: int, world_size: int, capacity=None):
     offs = (ctypes.c_int64 * n)()
     cap = None
     if capacity is not None:
+        if len(capacity) != int(world_size):
+            raise ValueError(f"capacity has {len(capacity)} entries, world_size is {world_size}")
         cap = (ctypes.c_uint32 * len(capacity))(*[int(v) for v in capacity])
     _check(L.whale_splitfc_plan(int(num_classes), int(world_size), cap, counts, offs), "whale_splitfc_plan")
     return list(counts), list(offs)
@@ -130,6 +132,9 @@ def whale_splitfc_plan_mem(num_classes: int, world_size: int, capacity=None, mem
     n = max(int(world_size), 1)
     counts = (ctypes.c_int64 * n)()
     offs = (ctypes.c_int64 * n)()
+    for name, v in (("capacity", capacity), ("mem_bytes", mem_bytes)):
+        if v is not None and len(v) != int(world_size):
+            raise ValueError(f"{name} has {len(v)} entries, world_size is {world_size}")
     cap = None if capacity is None else (ctypes.c_uint32 * len(capacity))(*[int(v) for v in capacity])
     mem = None if mem_bytes is None else (ctypes.c_uint64 * len(mem_bytes))(*[int(v) for v in mem_bytes])
     _check(L.whale_splitfc_plan_mem(int(num_classes), int(world_size), cap, mem, int(bytes_per_class),

@@ -15,6 +15,14 @@
 //   warp 2      TMEM allocator
 //   warps 4..7  epilogue: fp32 tile -> swizzled smem -> one 128-row TMA store per 32
 //               columns; dX units then run the split-K fixup (gemm_sm100.cuh)
+//   warps 8..11 G-fused mode (NEXT-4b): operand transformers.  The A stages
+//               of both GEMMs hold P~ = e^{z - m_tile} (the forward's bf16 output); each
+//               thread turns one 128-byte smem row of a landed stage into
+//               G = (P~ e^{m_tile - lse} / B_tot) - onehot / B_tot  (PAPER.md:286-288,
+//               the softmax-minus-onehot gradient) before the MMA reads it, so G never
+//               exists in HBM.  Every smem row of an A stage has ONE factor: a dX stage is
+//               128 batch rows x 64 classes of one forward class tile (K-major); a dW stage
+//               is 2 boxes x bk batch rows x 64 classes (MN-major G^T), again one tile per box.
 #pragma once
 #include "gemm_sm100.cuh"
 
@@ -39,6 +47,15 @@ struct CombineArgs {
   int rank, world, Bslab;
 };
 
+// G-fused operand path: A stages hold P~; G[i, j] = P~[i, j] gscale[i, j / fwd_bn] - [j == y_i - o_r] / B_tot
+struct GFuse {
+  const float* gscale;  // [T x Bt] e^{m_tile - lse} / B_tot (statistics kernel), NULL: A holds G already
+  const int32_t* y;     // [Bt] global labels
+  long long o_r, C_r;
+  int T, fwd_bn, Bt;
+  float inv_bt;
+};
+
 struct BwdArgs {
   GemmArgs dx;          // units [0, ux): M = B_tot, N = D, K = C_r (A = G K-major, B = W_r MN-major)
   GemmArgs dw;          // units [ux, ux + tw): M = C_r, N = D, K = B_tot (both MN-major)
@@ -46,9 +63,35 @@ struct BwdArgs {
   int tc;               // F1 dX combine units (no TMEM / smem stages), scheduled FIRST: unit ids
                         // [0, tc) are combine units and the GEMM units above are shifted by tc
   CombineArgs cb;
+  GFuse gf;
   int stages, stage_bytes, epi_bufs;  // epi_bufs: CTA-wide 16 KB store stages
-  unsigned* sched_cnt;  // monotonic dynamic-scheduler counter: (e - 1) * (ux + tw + tc) at launch
+  unsigned* sched_cnt;  // dynamic-scheduler counter (zeroed by the last CTA of every launch)
 };
+
+constexpr int kBwdThreads = 384;  // 12 warps (8..11: G-fused operand transformers)
+
+// One 128-byte SW128 smem row (8 x 16-byte chunks, chunk c stored at c ^ (row & 7)) of P~,
+// all in one forward class tile: G = P~ * sc - [class == oc] / B_tot, rounded to bf16 as the
+// in-place rewrite does (same expression, so G is bit-identical to the materialised one).
+__device__ __forceinline__ void gfuse_row(uint8_t* row, int rsw, float sc, long long oc, float inv_bt) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {  // logical chunk q (classes 8q .. 8q + 7) sits at chunk q ^ rsw:
+    // walking logical chunks spreads the 32 lanes (32 rows) over all banks
+    uint8_t* cp = row + ((q ^ rsw) << 4);
+    uint4 raw = *reinterpret_cast<const uint4*>(cp);
+    const int c0 = q << 3;  // first class (within the 64) of this chunk
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 f = __bfloat1622float2(h[k]);
+      const long long j = c0 + 2 * k;
+      f.x = f.x * sc - ((j == oc) ? inv_bt : 0.f);
+      f.y = f.y * sc - ((j + 1 == oc) ? inv_bt : 0.f);
+      h[k] = __floats2bfloat162_rn(f.x, f.y);
+    }
+    *reinterpret_cast<uint4*>(cp) = raw;
+  }
+}
 
 constexpr int kCombineCols = 1024;  // dX columns per combine unit (128 threads x 2 float4)
 
@@ -124,7 +167,7 @@ __device__ __forceinline__ void combine_unit(const CombineArgs& c, int u, float*
 constexpr int kSchedSlots = 4;
 
 template <int ES>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     splitfc_bwd_kernel(const __grid_constant__ CUtensorMap tmGx, const __grid_constant__ CUtensorMap tmW,
                        const __grid_constant__ CUtensorMap tmPart, const __grid_constant__ CUtensorMap tmGw,
                        const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmDW,
@@ -141,7 +184,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* sfull = tempty + 2;
   uint64_t* sempty = sfull + kSchedSlots;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sempty + kSchedSlots);
+  uint64_t* ready = sempty + kSchedSlots;  // G-fused: A stage transformed (4 warp arrivals)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ready + a.stages);
 
   constexpr int kBK = kRowBytes / ES;
   constexpr int kAtom = kRowBytes / ES;
@@ -149,6 +193,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int total = a.ux + a.tw + a.tc;
+  const bool xf = a.gf.gscale != nullptr;  // G-fused operand path
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
@@ -161,8 +206,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < kSchedSlots; ++i) {
       mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], 1 + 4);  // MMA thread + 4 epilogue warps
+      mbar_init(&sempty[i], 1 + 4 + (xf ? 4 : 0));  // MMA thread + 4 epilogue warps (+ 4 transformer warps)
     }
+    for (int i = 0; i < a.stages; ++i) mbar_init(&ready[i], 4);
     fence_mbar_init();
   }
   if (threadIdx.x == 32) {
@@ -199,8 +245,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int it = 0;; ++it) {
         const int slot = it % kSchedSlots;
         mbar_wait(&sempty[slot], ((it / kSchedSlots) & 1) ^ 1u);
-        if (it > 0)
-          unit = static_cast<int>(atomicAdd(a.sched_cnt, 1u) - (e - 1u) * static_cast<uint32_t>(total)) + gridDim.x;
+        if (it > 0) unit = static_cast<int>(atomicAdd(a.sched_cnt, 1u)) + gridDim.x;
         if (unit >= total) unit = -1;
         sched_tile[slot] = unit;
         mbar_arrive(&sfull[slot]);
@@ -273,7 +318,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kMaxBN;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait(xf ? &ready[stage] : &full[stage], phase);
           tc_fence_after();
           const uint32_t aS = smem_u32(smem + stage * a.stage_bytes);
           if (is_dx) {
@@ -301,7 +346,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         umma_commit(&tfull[acc]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 8) {
     // ===================== epilogue =====================
     const int q = warp & 3;
     const int nbuf = a.epi_bufs;
@@ -362,10 +407,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         uint32_t* cnt = a.dx.tile_cnt + mb * a.dx.n_blocks + nb;
         if (threadIdx.x == 128) {
           atomicAdd(cnt, 1u);
-          const uint32_t target = e * static_cast<uint32_t>(a.dx.splits);
+          const uint32_t target = static_cast<uint32_t>(a.dx.splits);
           if (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0) {
             SpinGuard sg;
-            while (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0) sg.check(a.dx.err, 16);
+            while (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0)
+              if (sg.expired(a.dx.err, ERR_SPLITK)) break;
           }
         }
         named_bar_sync(1, 128);
@@ -374,6 +420,107 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
     if (threadIdx.x == 128) bulk_wait<0>();
+  } else if (warp >= 8 && xf) {
+    // ===================== G-fused operand transformers =====================
+    // thread tt owns one 128-byte row of every A stage.  The stages are walked as a task
+    // stream (unit by unit through the scheduler ring); the factor and label of task k + 2
+    // are loaded while task k is transformed, so the L2 latency of those loads is hidden.
+    // (Looking 2 tasks ahead is safe: the producer issues a unit's stages before it publishes
+    // the next unit, and at most 2 < ring-depth stages are held here untransformed.)
+    const int tt = threadIdx.x - 256;
+    const GFuse& g = a.gf;
+    const int dw_bk = a.dw.bk;
+    const int dw_box = dw_bk * kRowBytes;
+    int it = 0;           // scheduler-ring slots read
+    int u_kb = 0, u_kb1 = 0, u_dx = 0, u_mb = 0;  // current unit: remaining k-blocks [u_kb, u_kb1)
+    int t_stage = 0;      // smem stage of the next task
+    bool done = false;
+    struct Task {
+      int stage;
+      int row_off;        // byte offset of this thread's row in the stage, -1: no row
+      int rsw;
+      const float* sc;    // factor address (gscale, transposed [T x B_tot])
+      const int32_t* y;   // label address
+      long long cls0;     // first class of the row's 64
+      bool end;
+    };
+    auto next_task = [&]() -> Task {
+      Task k{};
+      while (u_kb >= u_kb1) {  // next GEMM unit from the scheduler ring
+        if (done) {
+          k.end = true;
+          return k;
+        }
+        const int slot = it % kSchedSlots;
+        mbar_wait(&sfull[slot], (it / kSchedSlots) & 1);
+        const int unit = sched_tile[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[slot]);
+        ++it;
+        if (unit < 0) {
+          done = true;
+          continue;
+        }
+        if (unit < a.tc) continue;  // combine unit: no operand stages
+        const int gu = unit - a.tc;
+        int nb, sp;
+        u_dx = gu < a.ux;
+        if (u_dx) decode_tile(a.dx, gu, u_mb, nb, sp, u_kb, u_kb1);
+        else decode_tile(a.dw, gu - a.ux, u_mb, nb, sp, u_kb, u_kb1);
+      }
+      const int kb = u_kb++;
+      k.stage = t_stage;
+      if (++t_stage == a.stages) t_stage = 0;
+      k.row_off = -1;
+      if (u_dx) {  // dX: A = G [batch rows x 64 classes]; row tt = batch row mb * 128 + tt
+        const int i = u_mb * kBM + tt;
+        if (i < g.Bt) {
+          k.row_off = tt * kRowBytes;
+          k.rsw = tt & 7;
+          k.cls0 = static_cast<long long>(kb) * kBK;
+          k.sc = g.gscale + static_cast<size_t>(k.cls0 / g.fwd_bn) * g.Bt + i;
+          k.y = g.y + i;
+        }
+      } else {  // dW: A = G^T MN-major, boxes {64 classes, bk batch rows}; row tt = (box j, row ii)
+        const int j = tt / dw_bk, ii = tt % dw_bk;
+        const long long cls0 = static_cast<long long>(u_mb) * kBM + j * kAtom;
+        const int i = kb * dw_bk + ii;
+        if (j < kBM / kAtom && cls0 < g.C_r && i < g.Bt) {
+          k.row_off = j * dw_box + ii * kRowBytes;
+          k.rsw = ii & 7;
+          k.cls0 = cls0;
+          k.sc = g.gscale + static_cast<size_t>(cls0 / g.fwd_bn) * g.Bt + i;
+          k.y = g.y + i;
+        }
+      }
+      return k;
+    };
+    // task ring of depth 3 kept in registers (rotated, never indexed dynamically)
+    Task k0 = next_task(), k1 = next_task();
+    const bool v0 = !k0.end && k0.row_off >= 0, v1 = !k1.end && k1.row_off >= 0;
+    float s0 = v0 ? __ldg(k0.sc) : 0.f, s1 = v1 ? __ldg(k1.sc) : 0.f;
+    int32_t y0 = v0 ? __ldg(k0.y) : 0, y1 = v1 ? __ldg(k1.y) : 0;
+    uint32_t phase = 0;
+    for (bool first = true; !k0.end; first = false) {
+      const Task k2 = next_task();  // prefetch two tasks ahead
+      const bool v2 = !k2.end && k2.row_off >= 0;
+      const float s2 = v2 ? __ldg(k2.sc) : 0.f;
+      const int32_t y2 = v2 ? __ldg(k2.y) : 0;
+      if (!first && k0.stage == 0) phase ^= 1u;
+      mbar_wait(&full[k0.stage], phase);
+      if (k0.row_off >= 0)
+        gfuse_row(smem + k0.stage * a.stage_bytes + k0.row_off, k0.rsw, s0, static_cast<long long>(y0) - g.o_r - k0.cls0,
+                  g.inv_bt);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ready[k0.stage]);
+      k0 = k1;
+      s0 = s1;
+      y0 = y1;
+      k1 = k2;
+      s1 = s2;
+      y1 = y2;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -381,7 +528,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, kTmemCols);
   }
-  end_of_step_ticket(a.dx, e, s_fix_go);  // RS flags (N > 1) + epoch++ (last CTA)
+  end_of_step_ticket(a.dx, e, s_fix_go, a.sched_cnt);  // RS flags (N > 1) + epoch publish + counter reset
 }
 
 }  // namespace whale

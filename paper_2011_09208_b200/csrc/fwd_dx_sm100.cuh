@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
     // ===================== TMA producers: warp 0 -> ring 1 (G1), warp 3 -> ring 2 (G2) =====
     if (lane == 0) {
       if (a.wait_flags != nullptr) {
-        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, 8);
+        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
         fence_proxy_async_global();
       }
       // L2 policy: G1 reads keep their lines (evict_last) until G2 re-reads them two periods
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
             }
           }
         }
-      } else if (!(a.debug & 2)) {  // debug bit 2: timing experiment without G2
+      } else if (!WHALE_SKIP(a.debug & 2)) {  // debug bit 2: timing experiment without G2
         for (int it = 0; it < my_tiles; ++it) {
           const int row0 = (cl + it * ncl) * kF1TileC;
           for (int m = 0; m < KQ / 2; ++m) {
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
       // G2 re-reads W about one period after G1 brought it into L2 (short reuse distance).
       // G2 order, and hence U's summation order, is fixed.
       for (int p = 0; p <= my_tiles; ++p) {
-        const bool has1 = p < my_tiles, has2 = p >= 1 && !(a.debug & 2);
+        const bool has1 = p < my_tiles, has2 = p >= 1 && !WHALE_SKIP(a.debug & 2);
         if (dbg && p < 64) g_f1_ts[p * 16 + 0] = gtime_ns();
         const int zb = p % 3;
         const int j = p - 1;  // G2 tile
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
             tc_fence_after();
             const uint32_t aS = r1 + s1 * kF1G1SlotBytes;
             const uint32_t bS = aS + kF1StageBytes;
-            if (a.debug & 8) {  // timing experiment: consume the slot without MMAs
+            if (WHALE_SKIP(a.debug & 8)) {  // timing experiment: consume the slot without MMAs
               mbar_arrive(&empty1[s1]);
             } else {
 #pragma unroll
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
             }
           }
           if (i == KQ / 2 - 1) {
-            if (a.debug & 8) mbar_arrive(&zfull[zb]);
+            if (WHALE_SKIP(a.debug & 8)) mbar_arrive(&zfull[zb]);
             else umma_commit(&zfull[zb]);
             if (dbg && p < 64) g_f1_ts[p * 16 + 1] = gtime_ns();
           }
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
             tc_fence_after();
           }
           while (g2_next < KQ / 2) g2_block(j, g2_next++);
-          if (a.debug & 8) mbar_arrive(&pempty[j & 1]);
+          if (WHALE_SKIP(a.debug & 8)) mbar_arrive(&pempty[j & 1]);
           else umma_commit(&pempty[j & 1]);
         } else if (p >= 1) {  // debug bit 2: G2 skipped, keep the P~ buffer protocol alive
           mbar_wait(&pfull[j & 1], pf_par);
@@ -341,6 +341,13 @@ __global__ void __launch_bounds__(kF1Threads, 1)
     const bool store_role = (qd % kF1KC) == static_cast<int>(q);  // one CTA stores each class row
     constexpr float kL2e = 1.4426950408889634f;
     constexpr int kE = kF1EpiThreads;
+    // N > 1: the gathered labels were stored by the peers' bridge_gather (generic stores +
+    // fence.sc.sys + flag increments): acquire those flags before reading them (the producer
+    // lanes' acquire does not order this thread's loads); the CTA barrier then orders the
+    // other epilogue threads' label reads after it.
+    if (a.wait_flags != nullptr && et == 0)
+      for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
+    named_bar_sync(2, kE);
     if (et < 32) {
       s_lab[et] = et < a.Bt ? a.labels[et] : -1;
       s_ref[et] = -INFINITY;
@@ -355,7 +362,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
       const long long cls = static_cast<long long>(t) * kF1TileC + cl_row;  // shard-local class
       const bool valid = cls < a.C_r;
       const bool dbg = (a.debug & 1) && blockIdx.x == 0 && et == 0 && it < 64;
-      if (a.debug & 4) {  // timing experiment: epilogue does nothing
+      if (WHALE_SKIP(a.debug & 4)) {  // timing experiment: epilogue does nothing
         mbar_wait(&zfull[zb], (it / 3) & 1);
         mbar_arrive(&zempty[zb]);
         if (it >= 2) mbar_wait(&pempty[it & 1], ((it >> 1) & 1) ^ 1u);

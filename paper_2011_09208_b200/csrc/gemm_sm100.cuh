@@ -78,13 +78,14 @@ struct GemmArgs {
   // split-K fixup (EPI_STORE_F32, dX)
   int fix_mode;             // FixMode
   const float* part;        // [splits x M x N] fp32 partials (the tmOut tensor)
-  uint32_t* tile_cnt;       // [m_blocks x n_blocks] monotonic arrival counters
-  uint32_t* done_cnt;       // monotonic end-of-kernel ticket (CTAs)
+  uint32_t* tile_cnt;       // [m_blocks x n_blocks] split-K arrival counters (re-armed by the end ticket)
+  uint32_t* done_cnt;       // end-of-launch ticket (CTAs; re-armed by the last CTA)
   void* out;                // FIX_LOCAL: final dX [M x N] (ES-sized elements)
   int B, rank, world;       // FIX_PUSH: B = slab rows per source rank (B_max)
   int row_off[kMaxRanks + 1];  // FIX_PUSH: rows [row_off[r], row_off[r+1]) belong to rank r
   PeerPtrs recv;            // FIX_PUSH: owner's fp32 slab [world][B x N]
-  PeerFlags rs_flags;       // FIX_PUSH: &flag[RS][rank] on every rank
+  PeerFlags rs_flags;       // N > 1: &flag[RS][rank] on every rank
+  int rs_signal;            // 1: this launch ends the step at N > 1 -> raise the RS flags
   int store_mode;           // EPI_STORE_F32: 0 per-warp TMA box, 1 CTA-wide TMA box, 2 st.global
   int n_fastest;            // tile order: 0 = M fastest (share B), 1 = N fastest (share A)
   int cluster;              // 1, or 2: CTA pairs take M-adjacent tiles and TMA-multicast B
@@ -204,22 +205,32 @@ __device__ __forceinline__ void fixup_share(const GemmArgs& a, int mb, int nb, i
   }
 }
 
-// End of the backward's last GEMM launch (after the CTA-wide __syncthreads): the last CTA
-// to finish raises flag[RS] = e on every rank (N > 1: all of this rank's dX pushes have
-// landed AND every CTA finished reading the gathered X, so peers may overwrite it next
-// step) and publishes the step epoch for the following kernels.
-__device__ __forceinline__ void end_of_step_ticket(const GemmArgs& a, uint32_t e, int& s_last) {
+// End of the backward's last launch (after the CTA-wide __syncthreads): the last CTA to
+// finish raises flag[RS] = e on every rank (N > 1: all of this rank's dX pushes have landed
+// AND every CTA finished reading the gathered X, so peers may overwrite it next step),
+// re-arms the launch-local counters (done ticket, split-K tile counters, the dynamic
+// scheduler) for the next backward -- they depend on no epoch, so forward-only steps in
+// between are harmless -- and publishes the step epoch for the following kernels.
+__device__ __forceinline__ void end_of_step_ticket(const GemmArgs& a, uint32_t e, int& s_last,
+                                                   unsigned* sched_cnt = nullptr) {
   if (threadIdx.x == 0) {
     __threadfence_system();
     const uint32_t done = atomicAdd(a.done_cnt, 1u) + 1u;
-    s_last = (done == e * gridDim.x);
+    s_last = (done == gridDim.x);
   }
   __syncthreads();
   if (!s_last) return;
   __threadfence_system();
-  if (threadIdx.x < a.world && a.fix_mode == FIX_PUSH) st_relaxed_sys(a.rs_flags.p[threadIdx.x], e);  // fenced above
+  if (threadIdx.x < a.world && a.rs_signal) st_relaxed_sys(a.rs_flags.p[threadIdx.x], e);  // fenced above
+  if (a.tile_cnt != nullptr)
+    for (int k = threadIdx.x; k < a.m_blocks * a.n_blocks; k += blockDim.x) a.tile_cnt[k] = 0u;
   __syncthreads();
-  if (threadIdx.x == 0) atomicExch(a.dev_epoch, e);
+  if (threadIdx.x == 0) {
+    *a.done_cnt = 0u;
+    if (sched_cnt != nullptr) *sched_cnt = 0u;
+    __threadfence();
+    atomicExch(a.dev_epoch, e);
+  }
 }
 
 // ES = operand element size: 2 -> bf16 (kind::f16), 4 -> fp32 storage run as kind::tf32.
@@ -281,7 +292,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (a.wait_flags != nullptr) {
         // peers' rows of A were pushed over NVLink by generic-proxy stores; acquire their
         // flags, then order the async-proxy (TMA) reads after them.
-        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, 8);
+        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
         fence_proxy_async_global();
       }
       int stage = 0;
@@ -289,7 +300,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
       const int box_bytes = bk * kRowBytes;
       const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
-      const uint32_t tx = static_cast<uint32_t>(((a.debug & 8) ? 0 : a_bytes) +
+      const uint32_t tx = static_cast<uint32_t>((WHALE_SKIP(a.debug & 8) ? 0 : a_bytes) +
                                                 (B_MN ? (a.BN / kAtom) * box_bytes : a.BN * kRowBytes));
       for (int tile = unit0; tile < a.num_tiles; tile += ustride) {
         int mb, nb, sp, kb0, kb1;
@@ -299,7 +310,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* sA = smem + stage * a.stage_bytes;
           uint8_t* sB = sA + a_bytes;
           mbar_arrive_expect_tx(&full[stage], tx);
-          if (a.debug & 8) {
+          if (WHALE_SKIP(a.debug & 8)) {
             // timing experiment: A operand not loaded
           } else if (!A_MN) {
             tma_load_2d(sA, &tmA, &full[stage], kb * kBK, mb * kBM);
@@ -356,7 +367,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t aS = smem_u32(smem + stage * a.stage_bytes);
           const uint32_t bS = aS + a_bytes;
 #pragma unroll 4
-          for (int k = 0; k < ((a.debug & 4) ? 0 : kmma); ++k) {  // MMAs of 32 bytes of K
+          for (int k = 0; k < (WHALE_SKIP(a.debug & 4) ? 0 : kmma); ++k) {  // MMAs of 32 bytes of K
             const uint64_t ad = A_MN ? umma_sdesc(aS + k * kKStepMN, box_bytes, 1024)
                                      : umma_sdesc(aS + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_sdesc(bS + k * kKStepMN, box_bytes, 1024)
@@ -380,6 +391,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
+    if constexpr (EPI == EPI_FWD_STATS) {
+      // N > 1: the gathered labels are peer-written (bridge_gather); acquire the gather flags
+      // here too before any label read (the producer's acquire orders only its own lane)
+      if (a.wait_flags != nullptr && threadIdx.x == 128)
+        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
+      named_bar_sync(1, 128);
+    }
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int nbuf = a.epi_bufs;
     uint8_t* ebuf = epi_smem + q * nbuf * kEpiBufBytes;
@@ -400,7 +418,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           // CTA-wide 128-row box: all 4 warps fill one 16 KB stage, one thread stores it
           for (int c0 = 0; c0 < a.BN; c0 += 32) {
             uint32_t v[32];
-            if (!(a.debug & 2)) {
+            if (!WHALE_SKIP(a.debug & 2)) {
               tmem_ld32(tbase + c0, v);
               tmem_ld_wait();
             } else {
@@ -411,7 +429,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               tc_fence_before();
               mbar_arrive(&tempty[acc]);
             }
-            if (a.debug & 1) continue;
+            if (WHALE_SKIP(a.debug & 1)) continue;
             if (threadIdx.x == 128) bulk_wait_read_n(nbuf);
             named_bar_sync(1, 128);
             uint8_t* b = epi_smem + buf * 4 * kEpiBufBytes + (q * 32 + lane) * 128;
@@ -578,10 +596,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint32_t* cnt = a.tile_cnt + mb * a.n_blocks + nb;
           if (threadIdx.x == 128) {
             atomicAdd(cnt, 1u);
-            const uint32_t target = e * static_cast<uint32_t>(a.splits);
+            const uint32_t target = static_cast<uint32_t>(a.splits);
             if (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0) {
               SpinGuard g;
-              while (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0) g.check(a.err, 16);
+              while (static_cast<int32_t>(ld_acquire_gpu(cnt) - target) < 0)
+                if (g.expired(a.err, ERR_SPLITK)) break;
             }
           }
           named_bar_sync(1, 128);

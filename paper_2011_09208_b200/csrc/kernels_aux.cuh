@@ -21,7 +21,6 @@
 
 namespace whale {
 
-enum ErrBits : int { ERR_LABEL = 1, ERR_COMM = 8 };
 
 // debug timestamps (globaltimer ns) for latency experiments; read via whale_debug_timestamps
 __device__ unsigned long long g_dbg_ts[32];
@@ -68,12 +67,11 @@ __global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const in
                                      int64_t x_vecs /*B_r*row_bytes/16*/, int B, int row_off /*R_r*/,
                                      int64_t row_vecs /*row_bytes/16*/, int rank, int world,
                                      PeerPtrs dst_x /*slab base on each rank*/, PeerPtrs dst_y,
-                                     PeerFlags flags /*&flag[GATHER][rank] on each rank*/, uint32_t epoch,
-                                     int dbg) {
+                                     PeerFlags flags /*&flag[GATHER][rank] on each rank*/, int dbg) {
   const bool ts = (dbg & 16) && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1);
   const int tso = blockIdx.x == 0 ? 0 : 8;
   if (ts) g_dbg_ts[tso + 0] = globaltimer();
-  if (!(dbg & 4)) pdl_wait();
+  if (!WHALE_SKIP(dbg & 4)) pdl_wait();
   pdl_trigger();
   TraceScope _trace(0);
   if (ts) g_dbg_ts[tso + 1] = globaltimer();
@@ -83,7 +81,7 @@ __global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const in
     const uint4 val = __ldg(x_local + v);
 #pragma unroll
     for (int p = 0; p < kMaxRanks; ++p)
-      if (p < world && (!(dbg & 1) || p == rank)) reinterpret_cast<uint4*>(dst_x.p[p])[off_vec + v] = val;
+      if (p < world && (!WHALE_SKIP(dbg & 1) || p == rank)) reinterpret_cast<uint4*>(dst_x.p[p])[off_vec + v] = val;
   }
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x) {
     const int32_t y = y_local[i];
@@ -92,13 +90,12 @@ __global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const in
       if (p < world) reinterpret_cast<int32_t*>(dst_y.p[p])[row_off + i] = y;
   }
   // every block signals every peer itself (no last-block ticket): after the CTA barrier,
-  // one fence.sc.sys + a release increment per peer; peers wait for epoch * gridDim.x.
-  (void)epoch;
+  // one fence.sc.sys + a relaxed increment per peer; peers wait for epoch * gridDim.x.
   if (ts) g_dbg_ts[tso + 2] = globaltimer();
   __syncthreads();
   if (ts) g_dbg_ts[tso + 3] = globaltimer();
   if (threadIdx.x == 0) {
-    if (!(dbg & 2)) __threadfence_system();
+    if (!WHALE_SKIP(dbg & 2)) __threadfence_system();
     if (ts) g_dbg_ts[tso + 4] = globaltimer();
     for (int p = 0; p < world; ++p) red_add_relaxed_sys(flags.p[p], 1u);  // ordered by the fence
     if (ts) g_dbg_ts[tso + 5] = globaltimer();
@@ -114,9 +111,7 @@ struct StatsArgs {
   int T, Bt, B, rank, world;
   int row0;              // this rank's first row in the gathered batch (R_r); its rows: [row0, row0 + B)
   long long o_r, C_r, C;
-  PeerPtrs peer_stats;   // float4 [world x Bt] slab on each rank (this parity)
-  PeerFlags peer_flags;  // &flag[STATS][rank] on each rank
-  const uint32_t* my_flags;  // flag[STATS][0..world) on this rank
+  PeerPtrs peer_stats;   // LL-word slab [world x Bt x 4] on each rank (N > 1)
   const uint32_t* dev_epoch; // step epoch e = *dev_epoch + 1 (device-resident, graph-capturable)
   float4* my_stats;      // this rank's slab (N > 1)
   float* lse;            // [Bt]
@@ -126,6 +121,11 @@ struct StatsArgs {
   unsigned* counter;
   int* err;
   int grad_vecs;         // 16-byte vectors of P~ per thread in the fused gradient (chunk size)
+  int chunks;            // G-rewrite chunks per row (0 with gscale: the backward forms G itself)
+  // G-fused backward (NEXT-4b): instead of rewriting P~ into G, write the per-(row, tile)
+  // factor gscale[i, t] = e^{m_tile(i, t) - lse_i} / B_tot; the backward applies it (and the
+  // one-hot) to each P~ operand stage in shared memory.  NULL: rewrite P~ -> G in place.
+  float* gscale;         // [T x Bt] (tile-major) or NULL
   // NEXT-4 predictions (optional): top-1 class of each local row and its probability
   const int32_t* a_tile; // [Bt x T] argmax class per (row, tile) from the logits epilogue
   const float* mx_tile;  // [Bt x T] true tile maxima when m_tile holds references (F1), else NULL
@@ -170,17 +170,50 @@ __device__ __forceinline__ float block_sum128(float v, float* red) {
   return r;
 }
 
+// This rank's row statistics over its class tiles: m = row max (true tile maxima), s = sum
+// of the tile sums rescaled to m (identical on every CTA of the row: fixed order).
+__device__ __forceinline__ void row_stats(const StatsArgs& a, int i, float& m_out, float& s_out, float* red) {
+  const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
+  const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
+  const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : mt;  // true maxima
+  float mloc[8], sloc[8];
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int t = threadIdx.x + k * kStatsThreads;
+    mloc[k] = t < a.T ? __ldg(mt + t) : -INFINITY;
+    sloc[k] = t < a.T ? __ldg(st + t) : 0.f;
+    m = fmaxf(m, t < a.T ? __ldg(mx + t) : -INFINITY);
+  }
+  for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, __ldg(mx + t));
+  m = block_max128(m, red);
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += sloc[k] * __expf(mloc[k] - m);
+  for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) s += __ldg(st + t) * __expf(__ldg(mt + t) - m);
+  m_out = m;
+  s_out = block_sum128(s, red);
+}
+
+// G-fused mode: gscale[t, i] = e^{m_tile(i, t) - lse_i} / B_tot (the factor the in-place
+// rewrite would apply to P~; same expression, so G is bit-identical either way).  Stored
+// tile-major [T x B_tot]: the backward's transformer threads (consecutive batch rows) then
+// read consecutive words.
+__device__ __forceinline__ void write_gscale(const StatsArgs& a, int i, float l, float inv_bt) {
+  const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
+  for (int t = threadIdx.x; t < a.T; t += kStatsThreads)
+    a.gscale[static_cast<size_t>(t) * a.Bt + i] = __expf(__ldg(mt + t) - l) * inv_bt;
+}
+
 // ---------------------------------------------------------------- A4-A6 fused (N = 1)
 // With a single shard the statistics need no exchange, so the forward finishes with one
-// kernel: grid (chunks, B_tot); every CTA recomputes its row's lse from the class-tile
-// partials (T <= a few thousand floats, L2-resident), turns its chunk of P~ into
-// G = (P~ e^{m_tile - lse} - onehot) / B_tot in place, chunk 0 writes lse / row loss, and
-// the last CTA sums the mean loss in a fixed order.
+// kernel: grid (1 + rewrite CTAs, B_tot); CTA 0 of a row computes its lse from the class-tile
+// partials (T <= a few thousand floats, L2-resident), writes lse / row loss (and gscale in
+// the G-fused mode) and takes the mean-loss ticket; the other CTAs recompute the same lse and
+// turn chunks of P~ into G = (P~ e^{m_tile - lse} - onehot) / B_tot in place.
 constexpr int kGradVecs = 4;  // 16-byte vectors per thread
-// G_r[i, j] = P~[i, j] * e^{m_tile(i, j / BN) - lse_i} / B_tot - [j == y_i] / B_tot, in place over
-// this CTA's chunk of row i.  Loads are issued kU vectors at a time before any store (the
-// stores may alias later loads as far as the compiler knows, so a plain loop serialises
-// load -> store round trips).
+// Loads are issued kU vectors at a time before any store (the stores may alias later loads as
+// far as the compiler knows, so a plain loop serialises load -> store round trips).
 constexpr int kRowWriter = 32;  // thread that writes a row's lse / loss (warp 1: no peer stores)
 
 // Mean loss over the global batch: every row's chunk-0 CTA takes a ticket after writing its
@@ -252,31 +285,13 @@ __device__ __forceinline__ void grad_rewrite(const StatsArgs& a, void* P, long l
 template <int ES>
 __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsArgs a, void* P, long long ldp,
                                                                    int BN, float inv_bt) {
-  constexpr int V = 16 / ES;
   __shared__ float red[4];
   pdl_wait();
   pdl_trigger();
   TraceScope _trace(2);
   const int i = blockIdx.y;
-  const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
-  const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
-  const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : mt;  // true maxima
-  float mloc[8], sloc[8];
-  float m = -INFINITY;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int t = threadIdx.x + k * kStatsThreads;
-    mloc[k] = t < a.T ? __ldg(mt + t) : -INFINITY;
-    sloc[k] = t < a.T ? __ldg(st + t) : 0.f;
-    m = fmaxf(m, t < a.T ? __ldg(mx + t) : -INFINITY);
-  }
-  for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, __ldg(mx + t));
-  m = block_max128(m, red);
-  float s = 0.f;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) s += sloc[k] * __expf(mloc[k] - m);
-  for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) s += __ldg(st + t) * __expf(__ldg(mt + t) - m);
-  s = block_sum128(s, red);
+  float m, s;
+  row_stats(a, i, m, s, red);
   const float l = m + logf(s);
   const long long y = a.y[i];
   const long long yl = y - a.o_r;
@@ -290,132 +305,122 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_kernel(const StatsAr
   }
   if (a.pred_local != nullptr && blockIdx.x == 0) {  // top-1: first tile holding the row max
     __shared__ int redi[4];
+    const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : a.m_tile + static_cast<size_t>(i) * a.T;
     const int ts = argmax_tile(mx, a.T, m, redi);
     if (threadIdx.x == 0) {
       a.pred_local[i] = a.a_tile[static_cast<size_t>(i) * a.T + ts];
       if (a.prob_local) a.prob_local[i] = 1.f / s;  // e^{m - lse}
     }
   }
-  // ---- block 0 of a row: the row's results and the mean-loss ticket only; blocks >= 1
-  //      rewrite G chunk blockIdx.x - 1 (keeps the ticket's fence off the rewrite path)
+  // ---- CTA 0 of a row: the row's results (+ gscale) and the mean-loss ticket only; CTAs
+  //      >= 1 rewrite G chunks blockIdx.x - 1, + (gridDim.x - 1), ... (keeps the ticket's
+  //      fence off the rewrite path)
   if (blockIdx.x == 0) {
+    if (a.gscale) write_gscale(a, i, l, inv_bt);
     mean_loss_ticket(a);
     return;
   }
-  grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, blockIdx.x - 1, mt, l, yl);
+  const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
+  for (int c = blockIdx.x - 1; c < a.chunks; c += gridDim.x - 1) grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, c, mt, l, yl);
 }
 
 // ---------------------------------------------------------------- A4-A6 fused (N > 1)
-// grid (B_tot rows, chunks): x = row so every row's chunk-0 CTA is dispatched first.
-// Each CTA reduces its row's local class tiles to (m_r, s_r); the chunk-0 CTA also takes
-// z_y,r and pushes the float4 record into every peer's slab [rank][row] followed by a
-// per-row release flag.  Every CTA of the row then acquires the world flags of its row,
-// combines the records in rank order (identical bits on every rank and every chunk CTA),
-// and turns its chunk of P~ into G.  Chunk 0 writes lse / row loss; the last CTA (local
-// ticket) sums the mean loss in a fixed order.
+// grid (row CTAs, 1 + rewrite CTAs); a row CTA x serves rows x, x + gridDim.x, ... (one row
+// each when gridDim.x = B_tot; fewer CTAs when ranks share a device, so only a few CTAs spin).
+// Phase 1 (y = 0): for each of its rows, reduce this rank's class tiles to (m_r, s_r), take
+// z_y,r and the top-1 class and push the record {m_r, s_r, z_y,r, top-1} as LL words into
+// every peer's slab [rank][row] -- no waiting in this phase, so every record of every rank
+// is eventually pushed whatever order CTAs run in.  Phase 2 (all CTAs): for each row, wait
+// for the world records, combine them in rank order (identical bits on every rank and
+// every CTA); y = 0 writes lse / row loss (and gscale in the G-fused mode) and takes the
+// mean-loss ticket (the last row sums the mean in a fixed order); y >= 1 (rewrite mode)
+// turns chunks y - 1, y - 1 + (gridDim.y - 1), ... of P~ into G.
 template <int ES>
 __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const StatsArgs a, void* P, long long ldp,
-                                                                         int BN, float inv_bt,
-                                                                         PeerFlags row_flags /*peer p: &rf[rank*Bt]*/,
-                                                                         const uint32_t* my_row_flags /*[world*Bt]*/) {
-  constexpr int V = 16 / ES;
+                                                                         int BN, float inv_bt) {
   __shared__ float red[4];
   __shared__ float4 recs[kMaxRanks];
+  __shared__ int redi[4];
   pdl_wait();
   pdl_trigger();
   TraceScope _trace(2);
-  const int i = blockIdx.x;
-  const int chunk_id = blockIdx.y;
+  const int cta = blockIdx.y;
   const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;
-  const int tslot = (g_trace_on && chunk_id == 0 && threadIdx.x == 0) ? (i == 0 ? 16 : (i == a.Bt - 1 ? 24 : -1)) : -1;
-  if (tslot >= 0) g_dbg_ts[tslot] = gtime_ns();
-  const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
-  const float* st = a.s_tile + static_cast<size_t>(i) * a.T;
-  const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : mt;  // true maxima
-  const long long y = a.y[i];
-  const long long yl = y - a.o_r;
-  if (chunk_id == 0) {
-    float mloc[8], sloc[8];
-    float m = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int t = threadIdx.x + k * kStatsThreads;
-      mloc[k] = t < a.T ? __ldg(mt + t) : -INFINITY;
-      sloc[k] = t < a.T ? __ldg(st + t) : 0.f;
-      m = fmaxf(m, t < a.T ? __ldg(mx + t) : -INFINITY);
+  if (cta == 0) {
+    for (int i = blockIdx.x; i < a.Bt; i += gridDim.x) {
+      const int tslot = (g_trace_on && threadIdx.x == 0) ? (i == 0 ? 16 : (i == a.Bt - 1 ? 24 : -1)) : -1;
+      if (tslot >= 0) g_dbg_ts[tslot] = gtime_ns();
+      const long long y = a.y[i];
+      float m, s;
+      row_stats(a, i, m, s, red);
+      if (tslot >= 0) g_dbg_ts[tslot + 1] = gtime_ns();
+      const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : a.m_tile + static_cast<size_t>(i) * a.T;
+      const int top = argmax_tile(mx, a.T, m, redi);  // this rank's top-1 tile for the row
+      const int top_class = a.a_tile[static_cast<size_t>(i) * a.T + top];
+      if (threadIdx.x < a.world) {  // thread p pushes the record to peer p
+        if (threadIdx.x == 0 && (y < 0 || y >= a.C)) atomicOr(a.err, ERR_LABEL);
+        const bool own = (y >= a.o_r) && (y < a.o_r + a.C_r);
+        const float zy = own ? a.zy_r[i] : 0.f;
+        const int p = threadIdx.x;
+        // LL-style: four 8-byte {value, epoch} words; each 8-byte store is single-copy atomic,
+        // so the reader validates every word by its epoch half -- no fence, no separate flag
+        uint2* dst = reinterpret_cast<uint2*>(a.peer_stats.p[p]) + (static_cast<size_t>(a.rank) * a.Bt + i) * 4;
+        st_relaxed_sys_v2(dst + 0, __float_as_uint(m), e);
+        st_relaxed_sys_v2(dst + 1, __float_as_uint(s), e);
+        st_relaxed_sys_v2(dst + 2, __float_as_uint(zy), e);
+        st_relaxed_sys_v2(dst + 3, static_cast<uint32_t>(top_class), e);
+      }
+      if (tslot >= 0) g_dbg_ts[tslot + 2] = gtime_ns();
     }
-    for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads) m = fmaxf(m, __ldg(mx + t));
-    m = block_max128(m, red);
-    float s = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) s += sloc[k] * __expf(mloc[k] - m);
-    for (int t = threadIdx.x + 8 * kStatsThreads; t < a.T; t += kStatsThreads)
-      s += __ldg(st + t) * __expf(__ldg(mt + t) - m);
-    s = block_sum128(s, red);
-    if (tslot >= 0) g_dbg_ts[tslot + 1] = gtime_ns();
-    __shared__ int redi[4];
-    const int top = argmax_tile(mx, a.T, m, redi);  // this rank's top-1 tile for the row
-    const int top_class = a.a_tile[static_cast<size_t>(i) * a.T + top];
-    if (threadIdx.x < a.world) {  // thread p pushes the record to peer p
-      if (threadIdx.x == 0 && (y < 0 || y >= a.C)) atomicOr(a.err, ERR_LABEL);
-      const bool own = (y >= a.o_r) && (y < a.o_r + a.C_r);
-      const float zy = own ? a.zy_r[i] : 0.f;
-      const int p = threadIdx.x;
-      // LL-style: three 8-byte {value, epoch} words; each 8-byte store is single-copy atomic,
-      // so the reader validates every word by its epoch half -- no fence, no separate flag
-      uint2* dst = reinterpret_cast<uint2*>(a.peer_stats.p[p]) + (static_cast<size_t>(a.rank) * a.Bt + i) * 4;
-      st_relaxed_sys_v2(dst + 0, __float_as_uint(m), e);
-      st_relaxed_sys_v2(dst + 1, __float_as_uint(s), e);
-      st_relaxed_sys_v2(dst + 2, __float_as_uint(zy), e);
-      st_relaxed_sys_v2(dst + 3, static_cast<uint32_t>(top_class), e);
+  }
+  for (int i = blockIdx.x; i < a.Bt; i += gridDim.x) {
+    const int tslot = (g_trace_on && cta == 0 && threadIdx.x == 0) ? (i == 0 ? 16 : (i == a.Bt - 1 ? 24 : -1)) : -1;
+    // ---- the row's records from every rank, combined in rank order
+    if (threadIdx.x < a.world) {
+      const uint2* src = reinterpret_cast<const uint2*>(a.my_stats) + (static_cast<size_t>(threadIdx.x) * a.Bt + i) * 4;
+      const float mv = __uint_as_float(wait_ll(src + 0, e, a.err, ERR_COMM | ERR_AT_STATS));
+      const float sv = __uint_as_float(wait_ll(src + 1, e, a.err, ERR_COMM | ERR_AT_STATS));
+      const float zv = __uint_as_float(wait_ll(src + 2, e, a.err, ERR_COMM | ERR_AT_STATS));
+      const uint32_t cv = wait_ll(src + 3, e, a.err, ERR_COMM | ERR_AT_STATS);
+      recs[threadIdx.x] = make_float4(mv, sv, zv, __uint_as_float(cv));
     }
-    if (tslot >= 0) g_dbg_ts[tslot + 2] = gtime_ns();
-  }
-  // ---- acquire the row's records from every rank, combine in rank order
-  (void)row_flags;
-  (void)my_row_flags;
-  if (threadIdx.x < a.world) {
-    const uint2* src = reinterpret_cast<const uint2*>(a.my_stats) + (static_cast<size_t>(threadIdx.x) * a.Bt + i) * 4;
-    const float mv = __uint_as_float(wait_ll(src + 0, e, a.err, ERR_COMM));
-    const float sv = __uint_as_float(wait_ll(src + 1, e, a.err, ERR_COMM));
-    const float zv = __uint_as_float(wait_ll(src + 2, e, a.err, ERR_COMM));
-    const uint32_t cv = wait_ll(src + 3, e, a.err, ERR_COMM);
-    recs[threadIdx.x] = make_float4(mv, sv, zv, __uint_as_float(cv));
-  }
-  __syncthreads();
-  if (tslot >= 0) g_dbg_ts[tslot + 3] = gtime_ns();
-  float mm = -INFINITY;
-  int top_rank = 0;
-  for (int p = 0; p < a.world; ++p)
-    if (recs[p].x > mm) {  // strict: the lowest rank (= lowest class ids) wins ties
-      mm = recs[p].x;
-      top_rank = p;
+    __syncthreads();
+    if (tslot >= 0) g_dbg_ts[tslot + 3] = gtime_ns();
+    float mm = -INFINITY;
+    int top_rank = 0;
+    for (int p = 0; p < a.world; ++p)
+      if (recs[p].x > mm) {  // strict: the lowest rank (= lowest class ids) wins ties
+        mm = recs[p].x;
+        top_rank = p;
+      }
+    float ss = 0.f, zz = 0.f;
+    for (int p = 0; p < a.world; ++p) {
+      ss += recs[p].y * __expf(recs[p].x - mm);
+      zz += recs[p].z;  // exactly one rank owns the label; the others contribute 0
     }
-  float ss = 0.f, zz = 0.f;
-  for (int p = 0; p < a.world; ++p) {
-    ss += recs[p].y * __expf(recs[p].x - mm);
-    zz += recs[p].z;  // exactly one rank owns the label; the others contribute 0
+    const int32_t top_cls = static_cast<int32_t>(__float_as_uint(recs[top_rank].w));
+    __syncthreads();  // recs is reused by the next row
+    const float l = mm + logf(ss);
+    if (cta == 0) {
+      if (threadIdx.x == 0 && a.pred_local && i >= a.row0 && i < a.row0 + a.B) {
+        a.pred_local[i - a.row0] = top_cls;
+        if (a.prob_local) a.prob_local[i - a.row0] = 1.f / ss;  // e^{m - lse}
+      }
+      if (threadIdx.x == kRowWriter) {  // not a thread that pushed to peers
+        a.lse[i] = l;
+        a.row_loss_all[i] = l - zz;
+        if (a.row_loss_local && i >= a.row0 && i < a.row0 + a.B) a.row_loss_local[i - a.row0] = l - zz;
+      }
+      // gscale, then the mean-loss ticket (its fence covers only this CTA's row results)
+      if (a.gscale) write_gscale(a, i, l, inv_bt);
+      mean_loss_ticket(a);
+      if (tslot >= 0) g_dbg_ts[tslot + 4] = gtime_ns();
+    } else {
+      const float* mt = a.m_tile + static_cast<size_t>(i) * a.T;
+      const long long yl = static_cast<long long>(a.y[i]) - a.o_r;
+      for (int c = cta - 1; c < a.chunks; c += gridDim.y - 1) grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, c, mt, l, yl);
+    }
   }
-  const float l = mm + logf(ss);
-  if (chunk_id == 0 && threadIdx.x == 0 && a.pred_local && i >= a.row0 && i < a.row0 + a.B) {
-    a.pred_local[i - a.row0] = static_cast<int32_t>(__float_as_uint(recs[top_rank].w));
-    if (a.prob_local) a.prob_local[i - a.row0] = 1.f / ss;  // e^{m - lse}
-  }
-  if (chunk_id == 0 && threadIdx.x == kRowWriter) {  // not a thread that pushed to peers
-    a.lse[i] = l;
-    a.row_loss_all[i] = l - zz;
-    if (a.row_loss_local && i >= a.row0 && i < a.row0 + a.B) a.row_loss_local[i - a.row0] = l - zz;
-  }
-  // ---- mean loss (chunk-0 CTAs, before their G chunk so the ticket's fence covers only the
-  //      row-loss stores): the last one sums all rows in a fixed order
-  if (chunk_id == 0) mean_loss_ticket(a);
-  // ---- G for this CTA's chunk of the row
-  const bool tl = g_trace_on && threadIdx.x == 0 && i == a.Bt - 1 && chunk_id == static_cast<int>(gridDim.y) - 1;
-  if (tl) g_dbg_ts[21] = gtime_ns();
-  if (chunk_id == 0) return;  // the row's stats / exchange CTA rewrites no G chunk
-  grad_rewrite<ES>(a, P, ldp, BN, inv_bt, i, chunk_id - 1, mt, l, yl);
-  if (tslot >= 0) g_dbg_ts[tslot + 4] = gtime_ns();
-  if (tl) g_dbg_ts[22] = gtime_ns();
 }
 
 // ---------------------------------------------------------------- A8 dX reduce-scatter (owner)
@@ -431,7 +436,7 @@ __global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict
   TraceScope _trace(6);
   // the backward GEMM already published this step's epoch (end-of-step ticket)
   const uint32_t e = ld_acquire_gpu(dev_epoch);
-  if (threadIdx.x < world) wait_flag_geq(my_flags + threadIdx.x, e, err, ERR_COMM);
+  if (threadIdx.x < world) wait_flag_geq(my_flags + threadIdx.x, e, err, ERR_COMM | ERR_AT_RS);
   __syncthreads();
   __threadfence_system();
   const int64_t total = static_cast<int64_t>(B) * (D / 4);
@@ -456,13 +461,22 @@ __global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict
 }
 
 // ---------------------------------------------------------------- NEXT-4 bias gradient
-// db_r[j] = sum_i G_r[i, j] (the FC bias gradient; G already includes 1/B_tot).
+// db_r[j] = sum_i G_r[i, j] (the FC bias gradient; G already includes 1/B_tot).  In the
+// G-fused mode the buffer still holds P~ and G[i, j] = P~[i, j] gscale[i, j / BN] - [j == y_i
+// - o_r] / B_tot is formed here (the same arithmetic as the in-place rewrite).
 // Pass 1: grid (column vectors, 128-row chunks) -> part[chunk][j]; pass 2 sums the chunks
 // in order.  Both passes use fixed summation orders (deterministic).
 constexpr int kDbRows = 128;
+struct DbFused {
+  const float* gscale;   // [T x Bt] or NULL (buffer holds G)
+  const int32_t* y;      // [Bt]
+  long long o_r;
+  int T, BN;
+  float inv_bt;
+};
 template <int ES>
 __global__ void __launch_bounds__(128) bias_grad_part_kernel(const void* G, long long ldp, int Bt, long long C_r,
-                                                             float* part /*[chunks x C_r]*/) {
+                                                             float* part /*[chunks x C_r]*/, const DbFused fz) {
   constexpr int V = 16 / ES;
   pdl_wait();
   pdl_trigger();
@@ -472,21 +486,34 @@ __global__ void __launch_bounds__(128) bias_grad_part_kernel(const void* G, long
   float acc[V];
 #pragma unroll
   for (int k = 0; k < V; ++k) acc[k] = 0.f;
+  const int tile = static_cast<int>(j0 / (fz.BN > 0 ? fz.BN : 1));
 #pragma unroll 4
   for (int r = r0; r < r1; ++r) {
+    float g[V];
     if constexpr (ES == 2) {
       const uint4 raw = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(G) + r * ldp + j0));
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const float2 f = __bfloat1622float2(h[k]);
-        acc[2 * k] += f.x;
-        acc[2 * k + 1] += f.y;
+        g[2 * k] = f.x;
+        g[2 * k + 1] = f.y;
       }
     } else {
       const float4 f = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G) + r * ldp + j0));
-      acc[0] += f.x; acc[1] += f.y; acc[2] += f.z; acc[3] += f.w;
+      g[0] = f.x; g[1] = f.y; g[2] = f.z; g[3] = f.w;
     }
+    if (fz.gscale != nullptr) {  // P~ -> G, rounded to the operand type like the rewrite
+      const float sc = __ldg(fz.gscale + static_cast<size_t>(tile) * Bt + r);
+      const long long yl = static_cast<long long>(__ldg(fz.y + r)) - fz.o_r;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float v = g[k] * sc - ((j0 + k == yl) ? fz.inv_bt : 0.f);
+        g[k] = ES == 2 ? __bfloat162float(__float2bfloat16_rn(v)) : v;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < V; ++k) acc[k] += g[k];
   }
   float* o = part + static_cast<size_t>(blockIdx.y) * C_r + j0;
 #pragma unroll

@@ -9,26 +9,66 @@
 
 namespace whale {
 
+// Timing experiments that SKIP work (results wrong: no A loads, no MMAs, no stores, no
+// peer stores ...) exist only in builds with -DWHALE_TIMING_EXPERIMENTS (scripts/); the
+// product library compiles them out.  Timestamp-only debug modes stay runtime switches.
+#ifdef WHALE_TIMING_EXPERIMENTS
+#define WHALE_SKIP(bits) (bits)
+#else
+#define WHALE_SKIP(bits) 0
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// ------------------------------------------------------------------ spin guard
-// Every spin loop is bounded: a bug must trap (kernel error) rather than hang the box.
-__device__ __forceinline__ uint64_t clock_u64() {
-  uint64_t c;
-  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
-  return c;
+// ------------------------------------------------------------------ spin guards
+// Every spin loop is bounded (wall clock, %globaltimer).
+//  * Waits on OTHER ranks or other CTAs (flags, LL words, split-K counters) give up after
+//    g_wait_timeout_ns: they set the error bit in the workspace error word and return, the
+//    kernel finishes its (now meaningless) work and still raises its own flags, so peers
+//    are not left spinning; whale_splitfc_check() then reports WHALE_ERR_COMM.  Once the
+//    error word holds a wait-timeout bit, later waits of the same step give up at once.
+//  * Waits inside one CTA (mbarriers of the TMA / MMA pipelines) cannot time out unless
+//    the kernel itself is broken; those trap (after the peer timeout + 10 s, as they may
+//    legitimately sit behind a peer wait of the same kernel) instead of hanging.
+__device__ unsigned long long g_wait_timeout_ns = 300ull * 1000000000ull;  // set by whale_splitfc_create
+__device__ __forceinline__ unsigned long long wall_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
+// Error word bits (workspace; whale_splitfc_check decodes them).  A timed-out wait raises
+// ERR_COMM or ERR_SPLITK plus the bit of its site.
+enum ErrBits : int {
+  ERR_LABEL = 1,          // a label outside [0, C)
+  ERR_COMM = 8,           // a wait on another rank timed out
+  ERR_SPLITK = 16,        // a split-K fixup counter wait (this rank's own CTAs) timed out
+  ERR_AT_GATHER = 32,     //   ... on the bridge all-gather flags (logits / F1 kernel)
+  ERR_AT_STATS = 64,      //   ... on the statistics records (stats kernel)
+  ERR_AT_RS = 128,        //   ... on the dX reduce-scatter flags (owner reduce)
+};
+constexpr int kErrWaitMask = ERR_COMM | ERR_SPLITK;
 struct SpinGuard {
-  uint64_t start;
-  __device__ __forceinline__ SpinGuard() : start(clock_u64()) {}
-  __device__ __forceinline__ void check(int* err_word, int code) {
-    // ~20 s at 2 GHz; only evaluated on the slow path
-    if (clock_u64() - start > (1ull << 35)) {
+  unsigned long long start;
+  unsigned n = 0;
+  __device__ __forceinline__ SpinGuard() : start(wall_ns()) {}
+  // true: stop waiting (timed out now, or an earlier wait of this step already did)
+  __device__ __forceinline__ bool expired(int* err_word, int code) {
+    if ((++n & 63u) != 0u) return false;  // poll the clock / error word every 64 spins
+    if (err_word && (*reinterpret_cast<volatile int*>(err_word) & kErrWaitMask)) return true;
+    if (wall_ns() - start > *reinterpret_cast<volatile unsigned long long*>(&g_wait_timeout_ns)) {
       if (err_word) atomicOr(err_word, code);
-      __trap();
+      return true;
     }
+    return false;
+  }
+  // intra-CTA pipeline waits: a timeout is an internal bug -> trap
+  __device__ __forceinline__ void check_internal() {
+    if ((++n & 1023u) != 0u) return;
+    // a peer wait upstream may legitimately take the whole peer timeout first
+    if (wall_ns() - start > *reinterpret_cast<volatile unsigned long long*>(&g_wait_timeout_ns) + 10000000000ull)
+      __trap();
   }
 };
 
@@ -73,7 +113,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait(a, parity)) return;
   SpinGuard g;
-  while (!mbar_try_wait(a, parity)) g.check(nullptr, 0);
+  while (!mbar_try_wait(a, parity)) g.check_internal();
 }
 
 // ------------------------------------------------------------------ TMA
@@ -275,14 +315,15 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const void* p) 
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-// Spin until the LL word carries `flag`; returns its data half.
+// Spin until the LL word carries `flag`; returns its data half (on a timeout: whatever the
+// word holds, with `code` raised in the error word).
 __device__ __forceinline__ uint32_t wait_ll(const uint2* p, uint32_t flag, int* err_word, int code) {
   unsigned long long w = ld_relaxed_sys_u64(p);
   if (static_cast<uint32_t>(w >> 32) != flag) {
     SpinGuard g;
     do {
       __nanosleep(20);
-      g.check(err_word, code);
+      if (g.expired(err_word, code)) break;
       w = ld_relaxed_sys_u64(p);
     } while (static_cast<uint32_t>(w >> 32) != flag);
   }
@@ -293,13 +334,13 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// Wait until *p >= epoch (monotonic epochs); traps after the guard interval.
+// Wait until *p >= epoch (monotonic epochs); gives up (error word) after the wait timeout.
 __device__ __forceinline__ void wait_flag_geq(const uint32_t* p, uint32_t epoch, int* err_word, int code) {
   if (static_cast<int32_t>(ld_acquire_sys(p) - epoch) >= 0) return;
   SpinGuard g;
   while (static_cast<int32_t>(ld_acquire_sys(p) - epoch) < 0) {
     __nanosleep(40);  // many CTAs may poll: keep L2 / NVLink free for the incoming data
-    g.check(err_word, code);
+    if (g.expired(err_word, code)) return;
   }
 }
 
@@ -405,7 +446,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
   const uint32_t a = smem_u32(bar);
   if (mbar_try_wait_cluster(a, parity)) return;
   SpinGuard g;
-  while (!mbar_try_wait_cluster(a, parity)) g.check(nullptr, 0);
+  while (!mbar_try_wait_cluster(a, parity)) g.check_internal();
 }
 
 // 32 lanes x 32b, 32 consecutive columns <- 32 registers per thread.

@@ -186,6 +186,7 @@ struct Layout {
   size_t a_tile = 0, dbpart = 0;  // NEXT-4: per-(row, tile) top-1 class; bias-gradient partials
   size_t upart = 0, uref = 0;     // F1: per-cluster U = sum_t P~_t W_t partials and their row references
   size_t mx_tile = 0;             // F1: true per-(row, tile) maxima (m_tile holds the references)
+  size_t gscale = 0;              // G-fused backward: e^{m_tile - lse} / B_tot per (row, tile)
   size_t local_total = 0;
   // fp32 (kind::tf32) backward only: K-major transposed operands
   size_t XT = 0, GT = 0, WT = 0;
@@ -193,7 +194,7 @@ struct Layout {
   // symmetric buffer offsets (per parity for the slabs); world > 1 only
   // single-buffered: a rank overwrites a peer's slab only after that peer's end-of-step
   // ticket (RS flag) proved it finished reading it (see end_of_step_ticket)
-  size_t flags = 0, rowflags = 0, xg = 0, yg = 0, stats = 0, dxrecv = 0, symm_total = 0;
+  size_t flags = 0, xg = 0, yg = 0, stats = 0, dxrecv = 0, symm_total = 0;
 };
 
 enum FlagKind { FLAG_GATHER = 0, FLAG_STATS = 1, FLAG_RS = 2 };
@@ -402,6 +403,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   L.tile_cnt = take(static_cast<size_t>(p.dx.m_blocks) * p.dx.n_blocks * 4);
   L.a_tile = take(static_cast<size_t>(p.Bt) * T * 4);
   L.dbpart = take(static_cast<size_t>(cdiv(p.Bt, kDbRows)) * p.Cr * 4);
+  L.gscale = take(static_cast<size_t>(p.Bt) * T * 4);
   if (p.f1) {
     L.upart = take(static_cast<size_t>(p.f1_ncl) * p.Bt * p.D * 4);
     L.uref = take(static_cast<size_t>(p.f1_ncl) * p.Bt * 4);
@@ -417,7 +419,6 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   o = 0;
   if (p.world > 1) {
     L.flags = take(4 * kMaxRanks * 4);
-    L.rowflags = take(static_cast<size_t>(p.world) * p.Bt * 4);
     L.xg = take(static_cast<size_t>(p.Bt) * p.D * p.es);
     L.yg = take(p.Bt * 4);
     L.stats = take(static_cast<size_t>(p.world) * p.Bt * 32);  // LL words {m,s,zy,-} x {data, epoch}
@@ -529,6 +530,8 @@ struct whale_splitfc_ctx {
   bool have_fwd = false;
   bool pdl = true;
   bool fused_bwd = true;             // dW + dX in one persistent launch (bf16)
+  bool gfuse = true;                 // G-fused backward (NEXT-4b): G formed from P~ in the bwd operand path
+  bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
   std::vector<ProfRec> prof;
@@ -667,6 +670,40 @@ static GemmArgs base_args(const GemmCfg& g, int M, int N) {
     }                              \
   } while (0)
 
+// Load every kernel of the library into the current context now (CUDA lazy loading would
+// otherwise load a function at its first launch, and loading may wait for the device's
+// running kernels -- a deadlock when those kernels spin on flags that a not-yet-launched
+// kernel of another rank sharing the device must raise, and a latency spike mid-step).
+static whale_status_t preload_kernels() {
+  const void* fns[] = {
+      reinterpret_cast<const void*>(bridge_gather_kernel),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_FWD_STATS, false, false, 2>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_FWD_STATS, false, false, 4>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, true, true, 2>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, false, true, 2>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, false, false, 4>),
+      reinterpret_cast<const void*>(splitfc_fwd_dx_kernel),
+      reinterpret_cast<const void*>(splitfc_bwd_kernel<2>),
+      reinterpret_cast<const void*>(stats_grad_kernel<2>),
+      reinterpret_cast<const void*>(stats_grad_kernel<4>),
+      reinterpret_cast<const void*>(stats_grad_multi_kernel<2>),
+      reinterpret_cast<const void*>(stats_grad_multi_kernel<4>),
+      reinterpret_cast<const void*>(dx_reduce_kernel<2>),
+      reinterpret_cast<const void*>(dx_reduce_kernel<4>),
+      reinterpret_cast<const void*>(dx_combine_kernel<2>),
+      reinterpret_cast<const void*>(bias_grad_part_kernel<2>),
+      reinterpret_cast<const void*>(bias_grad_part_kernel<4>),
+      reinterpret_cast<const void*>(bias_grad_sum_kernel),
+      reinterpret_cast<const void*>(epoch_bump_kernel),
+      reinterpret_cast<const void*>(transpose_f32_kernel),
+  };
+  for (const void* f : fns) {
+    cudaFuncAttributes fa{};
+    CUDA_TRY(cudaFuncGetAttributes(&fa, f));
+  }
+  return WHALE_OK;
+}
+
 extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, whale_splitfc_ctx** out) {
   if (!out) return fail(WHALE_ERR_INVALID_ARG, "NULL out");
   *out = nullptr;
@@ -675,6 +712,10 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (major != 10) return fail(WHALE_ERR_UNSUPPORTED, "needs an sm_100 (B200) device, found major %d", major);
+  {
+    const whale_status_t pst = preload_kernels();
+    if (pst != WHALE_OK) return pst;
+  }
   auto* c = new whale_splitfc_ctx();
   whale_status_t st = build_plan(desc, c->p, sms);
   if (st != WHALE_OK) {
@@ -696,8 +737,19 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     for (int r = 0; r < p.world; ++r) c->symm[r] = static_cast<uint8_t*>(desc->peer_symm_ptrs[r]);
   }
   const char* pdl_env = getenv("WHALE_PDL");
-  c->pdl = !(pdl_env && pdl_env[0] == '0');
+  // WHALE_SHARED_DEVICE=1: several ranks share this device (the single-GPU multi-rank test
+  // harness): their kernels wait on one another, so no kernel may sit resident ahead of its
+  // turn (no PDL) and the exchange kernels keep bounded grids; combine with
+  // WHALE_SM_LIMIT_R<r> so every rank's persistent grid fits beside the others.
+  c->shared_device = env_int("WHALE_SHARED_DEVICE", 0) != 0;
+  c->pdl = !(pdl_env && pdl_env[0] == '0') && !c->shared_device;
+  {
+    // peer-wait timeout (flags, LL records, split-K counters): WHALE_TIMEOUT_MS, default 300 s
+    const unsigned long long ns = static_cast<unsigned long long>(std::max(1, env_int("WHALE_TIMEOUT_MS", 300000))) * 1000000ull;
+    CUDA_TRY(cudaMemcpyToSymbol(g_wait_timeout_ns, &ns, sizeof(ns)));
+  }
   c->fused_bwd = p.es == 2 && env_int("WHALE_FUSED_BWD", 1) != 0 && g_store_mode == 1;
+  c->gfuse = c->fused_bwd && env_int("WHALE_GFUSE", 0) != 0;
   if (c->fused_bwd) {
     // F1: the backward runs dW tiles only (dX came from the forward)
     c->bwd_stage_bytes = p.f1 ? p.dw.stage_bytes : std::max(p.dx.stage_bytes, p.dw.stage_bytes);
@@ -861,7 +913,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     PROFILED(K_GATHER, s,
              (launch(c, bridge_gather_kernel, dim3(grid), dim3(256), 0, s, static_cast<const uint4*>(x_local),
                      y_local, x_vecs, static_cast<int>(p.B), static_cast<int>(p.Boff[p.rank]),
-                     static_cast<int64_t>(p.D * ES / 16), p.rank, p.world, dx, dy, fl, 0u,
+                     static_cast<int64_t>(p.D * ES / 16), p.rank, p.world, dx, dy, fl,
                      env_int("WHALE_GATHER_DBG", 0))));
   }
   // ---- A3 logits GEMM with fused row statistics
@@ -930,7 +982,8 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
              (launch_gemm<EPI_FWD_STATS, false, false, ES>(c, ES == 2 ? 0 : 3, p.fwd, c->tmX_fwd,
                                                            c->tmW_fwd, c->tmP_store, a, s)));
   }
-  // ---- A4 + A5 statistics (exchange), combine, loss
+  // ---- A4 + A5 statistics (exchange), combine, loss; A6 either in place (P~ -> G) or, with
+  //      the G-fused backward, as the per-(row, tile) factor table the backward applies
   {
     StatsArgs a{};
     a.m_tile = wsp<float>(c, L.m_tile);
@@ -947,11 +1000,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.C_r = p.Cr;
     a.C = p.C;
     if (p.world > 1) {
-      for (int r = 0; r < p.world; ++r) {
-        a.peer_stats.p[r] = c->symm[r] + L.stats;
-        a.peer_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_STATS * kMaxRanks + p.rank;
-      }
-      a.my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_STATS * kMaxRanks;
+      for (int r = 0; r < p.world; ++r) a.peer_stats.p[r] = c->symm[r] + L.stats;
       a.my_stats = reinterpret_cast<float4*>(c->symm[p.rank] + L.stats);
     }
     a.dev_epoch = dev_epoch;
@@ -961,33 +1010,43 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.row_loss_local = row_loss;
     a.counter = counters + CNT_STATS;
     a.err = err;
-    // every CTA re-reads its row's T tile partials (8T bytes): size the chunk so that this
-    // stays <= ~10% of the chunk's P~ read+write traffic (4096 B per vector of the 128 threads)
     a.a_tile = wsp<int32_t>(c, L.a_tile);
     a.mx_tile = p.f1 ? wsp<float>(c, L.mx_tile) : nullptr;
     a.pred_local = pred;
     a.prob_local = prob;
+    // every rewrite CTA re-reads its row's T tile partials (8T bytes): size the chunk so that
+    // this stays <= ~10% of the chunk's P~ read+write traffic (4096 B per vector of the 128
+    // threads); F1 (B_tot <= 32, 128-class tiles): the re-read comes from L2 and the grid is
+    // short (B_tot rows) -> small chunks for enough loads in flight
     a.grad_vecs = static_cast<int>(std::min<int64_t>(64, std::max<int64_t>(4, (p.fwd.n_blocks * 10 + 511) / 512)));
-    // F1 (B_tot <= 32, 128-class tiles): the per-CTA partial re-read comes from L2 and the
-    // grid is short (B_tot rows) -> small chunks for enough loads in flight
     if (p.f1) a.grad_vecs = env_int("WHALE_F1_GV", 4);
     const int64_t chunk = static_cast<int64_t>(kStatsThreads) * a.grad_vecs * (16 / ES);
+    int gy = 1;  // CTAs per row: the statistics CTA (+ G-rewrite CTAs)
+    if (c->gfuse) {
+      a.gscale = wsp<float>(c, L.gscale);  // NEXT-4b: the backward forms G from P~ itself
+      a.chunks = 0;
+    } else {
+      a.chunks = cdiv(p.Cr, chunk);
+      // ranks sharing one device (emulation): keep the grid to a few CTAs per SM of this rank
+      const int cap = c->shared_device ? std::max(1, 2 * p.sms / static_cast<int>(p.Bt)) : a.chunks;
+      gy = 1 + std::max(1, std::min(a.chunks, cap));
+    }
+    const float inv_bt = static_cast<float>(1.0 / static_cast<double>(p.Bt));
+    void* P = static_cast<void*>(c->ws + L.P);
     if (p.world == 1) {
-      // A4-A6 fused: lse, loss and G in one pass (no exchange needed)
+      // A4-A6 fused: lse, loss and G (or its factors) in one pass (no exchange needed)
       PROFILED(K_STATS, s,
-               (launch(c, stats_grad_kernel<ES>, dim3(cdiv(p.Cr, chunk) + 1, p.Bt), dim3(kStatsThreads), 0, s, a,
-                       static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
-                       static_cast<float>(1.0 / static_cast<double>(p.Bt)))));
+               (launch(c, stats_grad_kernel<ES>, dim3(gy, p.Bt), dim3(kStatsThreads), 0, s, a, P,
+                       static_cast<long long>(p.ldp), p.fwd.BN, inv_bt)));
     } else {
       // A4-A6 fused with the per-row cross-GPU exchange (chunk-0 CTAs of every row first)
-      PeerFlags rf{};
-      for (int r = 0; r < p.world; ++r)
-        rf.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.rowflags) + static_cast<size_t>(p.rank) * p.Bt;
+      // one row per CTA; ranks sharing a device: a few row CTAs (they spin on the peers'
+      // records, and spinning CTAs must not crowd out the peers' persistent kernels)
+      const int gx = c->shared_device ? std::max(1, std::min(static_cast<int>(p.Bt), p.sms / 8)) : static_cast<int>(p.Bt);
+      if (c->shared_device) gy = std::min(gy, 2);
       PROFILED(K_STATS, s,
-               (launch(c, stats_grad_multi_kernel<ES>, dim3(p.Bt, cdiv(p.Cr, chunk) + 1), dim3(kStatsThreads), 0, s, a,
-                       static_cast<void*>(c->ws + L.P), static_cast<long long>(p.ldp), p.fwd.BN,
-                       static_cast<float>(1.0 / static_cast<double>(p.Bt)), rf,
-                       reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.rowflags))));
+               (launch(c, stats_grad_multi_kernel<ES>, dim3(gx, gy), dim3(kStatsThreads), 0, s, a, P,
+                       static_cast<long long>(p.ldp), p.fwd.BN, inv_bt)));
     }
   }
   return WHALE_OK;
@@ -1050,10 +1109,19 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     constexpr int V = 16 / ES;
     const int chunks = cdiv(p.Bt, kDbRows);
     float* part = wsp<float>(c, L.dbpart);
+    DbFused fz{};
+    if (c->gfuse) {  // the buffer still holds P~: form G on the fly (same arithmetic as the rewrite)
+      fz.gscale = wsp<float>(c, L.gscale);
+      fz.y = yg;
+      fz.o_r = p.o_r;
+      fz.T = p.fwd.n_blocks;
+      fz.BN = p.fwd.BN;
+      fz.inv_bt = static_cast<float>(1.0 / static_cast<double>(p.Bt));
+    }
     PROFILED(K_DB, s,
              (launch(c, bias_grad_part_kernel<ES>, dim3(cdiv(cdiv(p.Cr, V), 128), chunks), dim3(128), 0, s,
                      static_cast<const void*>(c->ws + L.P), static_cast<long long>(p.ldp), static_cast<int>(p.Bt),
-                     static_cast<long long>(p.Cr), part)));
+                     static_cast<long long>(p.Cr), part, fz)));
     PROFILED(K_DB, s,
              (launch(c, bias_grad_sum_kernel, dim3(std::max(1, std::min(cdiv(p.Cr, 256), 4 * p.sms))), dim3(256), 0,
                      s, static_cast<const float*>(part), chunks, static_cast<long long>(p.Cr), db)));
@@ -1067,6 +1135,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
   ax.done_cnt = counters + CNT_DONE;
   ax.dev_epoch = dev_epoch;
   ax.bump_epoch = 1;  // the dX launch (or the fused launch) ends the step
+  ax.rs_signal = p.world > 1 ? 1 : 0;
   ax.B = static_cast<int>(p.Bmax);
   for (int r = 0; r <= p.world; ++r) ax.row_off[r] = static_cast<int>(p.Boff[r]);
   ax.rank = p.rank;
@@ -1134,6 +1203,17 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       cb.Bslab = static_cast<int>(p.Bmax);
       b.tc = static_cast<int>(p.Bt) * cb.parts;
     }
+    if (c->gfuse) {  // NEXT-4b: the transformer warps turn each P~ operand stage into G
+      GFuse& gf = b.gf;
+      gf.gscale = wsp<float>(c, L.gscale);
+      gf.y = yg;
+      gf.o_r = p.o_r;
+      gf.C_r = p.Cr;
+      gf.T = p.fwd.n_blocks;
+      gf.fwd_bn = p.fwd.BN;
+      gf.Bt = static_cast<int>(p.Bt);
+      gf.inv_bt = static_cast<float>(1.0 / static_cast<double>(p.Bt));
+    }
     b.stages = c->bwd_stages;
     b.stage_bytes = c->bwd_stage_bytes;
     b.epi_bufs = c->bwd_epi_bufs;
@@ -1145,21 +1225,30 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       if (st != WHALE_OK) return st;
     }
     PROFILED(K_BWD, s,
-             (launch(c, kern, dim3(grid), dim3(kGemmThreads), c->bwd_smem, s, c->tmG_dx, c->tmW_dx, c->tmDxPart,
+             (launch(c, kern, dim3(grid), dim3(kBwdThreads), c->bwd_smem, s, c->tmG_dx, c->tmW_dx, c->tmDxPart,
                      c->tmG_dw, c->tmX_dw, c->tmDW, b)));
   } else if constexpr (ES == 2) {
-    // ---- A7 dW_r = G_r^T X  (A = G^T MN-major, B = X MN-major)
+    // ---- A7 dW_r = G_r^T X  (A = G^T MN-major, B = X MN-major); on the F1 path dX came from
+    //      the combine kernel above, so this launch ends the step
     {
       GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
       a.dev_epoch = dev_epoch;
       a.err = err;
       a.st_out = static_cast<float*>(dw);
+      if (p.f1) {
+        a.bump_epoch = 1;
+        a.done_cnt = ax.done_cnt;
+        a.rs_signal = ax.rs_signal;
+        a.rs_flags = ax.rs_flags;
+        a.world = p.world;
+      }
       PROFILED(K_DW, s,
                (launch_gemm<EPI_STORE_F32, true, true, 2>(c, 1, p.dw, c->tmG_dw, c->tmX_dw, c->tmDW, a, s)));
     }
     // ---- A8 dX = G_r W_r  (A = G K-major, B = W_r MN-major), split-K + fused fixup
-    PROFILED(K_DX, s,
-             (launch_gemm<EPI_STORE_F32, false, true, 2>(c, 2, p.dx, c->tmG_dx, c->tmW_dx, c->tmDxPart, ax, s)));
+    if (!p.f1)
+      PROFILED(K_DX, s,
+               (launch_gemm<EPI_STORE_F32, false, true, 2>(c, 2, p.dx, c->tmG_dx, c->tmW_dx, c->tmDxPart, ax, s)));
   } else {
     // kind::tf32 accepts K-major operands only (plain 128B swizzle): transpose G, X, W_r.
     const void* xg = p.world == 1 ? c->x_fwd : static_cast<const void*>(c->symm[p.rank] + L.xg);
@@ -1184,7 +1273,8 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
   // ---- A8 owner side of the reduce-scatter (N > 1)
   if (p.world > 1) {
     const int64_t own = p.B * p.D / 4;
-    const int g2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(own, 256), 2 * p.sms)));
+    const int g2 = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(cdiv(own, 256), c->shared_device ? std::max(1, p.sms / 8) : 2 * p.sms)));
     const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_RS * kMaxRanks;
     PROFILED(K_RS_REDUCE, s,
              (launch(c, dx_reduce_kernel<ES>, dim3(g2), dim3(256), 0, s,
@@ -1222,7 +1312,10 @@ extern "C" whale_status_t whale_splitfc_check(whale_splitfc_ctx* ctx, void* stre
   CUDA_TRY(cudaMemcpy(&h, err, sizeof(int), cudaMemcpyDeviceToHost));
   if (h) CUDA_TRY(cudaMemset(err, 0, sizeof(int)));
   if (h & ERR_LABEL) return fail(WHALE_ERR_LABEL, "a label is outside [0, C)");
-  if (h & (ERR_COMM | 16)) return fail(WHALE_ERR_COMM, "a peer / split-K flag wait timed out");
+  if (h & (ERR_COMM | ERR_SPLITK))
+    return fail(WHALE_ERR_COMM, "a wait timed out (error bits 0x%x:%s%s%s%s); destroy and re-create the context on every rank",
+                h, (h & ERR_AT_GATHER) ? " bridge-gather flags" : "", (h & ERR_AT_STATS) ? " statistics records" : "",
+                (h & ERR_AT_RS) ? " reduce-scatter flags" : "", (h & ERR_SPLITK) ? " split-K counters" : "");
   return WHALE_OK;
 }
 
@@ -1232,7 +1325,7 @@ extern "C" int32_t whale_splitfc_launches_per_step(const whale_splitfc_ctx* ctx)
   // N = 1: logits, stats+grad, dW, dX;  N > 1: + gather, + dX owner reduce
   int base = ctx->p.world == 1 ? 4 : 6;
   if (ctx->fused_bwd) base -= 1;  // dW + dX share one launch (F1: dW tiles + dX combine units)
-  else if (ctx->p.f1) base += 0;    // F1 unfused: the dX GEMM is replaced by the combine kernel
+  // F1 unfused: the combine kernel replaces the dX GEMM (same count)
   return base + (ctx->p.es == 4 ? 3 : 0);  // fp32 path: operand transposes
 }
 

@@ -5,8 +5,16 @@ context of libwhale_splitfc.so; ``forward``/``backward`` are the C-ABI calls on 
 torch stream.  For world > 1 the symmetric (peer-mapped) buffer comes from
 ``torch.distributed._symmetric_memory`` and all exchanges run in the library's own NVLink
 kernels; the process group is used only for the rendezvous and a barrier.
+
+``emulated_ranks`` builds N ranks on ONE device (the single-GPU test harness): the
+"symmetric" buffers are plain allocations every rank's context addresses directly, so the
+library's exchange kernels (bridge gather, statistics records, dX reduce-scatter) run
+unchanged, each rank on its own stream.
 """
 from __future__ import annotations
+
+import os
+from contextlib import contextmanager
 
 import torch
 
@@ -27,11 +35,13 @@ class SplitFCSoftmaxCE:
 
     def __init__(self, num_classes: int, feature_dim: int, local_batch: int, capacity=None,
                  dtype=torch.bfloat16, group=None, device=None, mem_bytes=None, bytes_per_class=None,
-                 batch_counts=None):
+                 batch_counts=None, emulated=None):
         self.C, self.D, self.B = int(num_classes), int(feature_dim), int(local_batch)
         self.dtype = dtype
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        if group is not None:
+        if emulated is not None:  # (rank, world, [world] uint8 device buffers): see emulated_ranks
+            self.rank, self.world = int(emulated[0]), int(emulated[1])
+        elif group is not None:
             import torch.distributed as dist
             self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
         else:
@@ -60,7 +70,13 @@ class SplitFCSoftmaxCE:
         self.workspace = torch.empty(local_bytes, dtype=torch.uint8, device=self.device)
         peer_ptrs = None
         self._symm = None
-        if self.world > 1:
+        if emulated is not None and self.world > 1:
+            bufs = emulated[2]
+            if len(bufs) != self.world or any(b.numel() < symm_bytes for b in bufs):
+                raise ValueError(f"emulated ranks need {self.world} buffers of >= {symm_bytes} bytes")
+            peer_ptrs = [int(b.data_ptr()) for b in bufs]
+            self._symm = bufs
+        elif self.world > 1:
             import torch.distributed as dist
             import torch.distributed._symmetric_memory as symm_mem
             buf = symm_mem.empty(symm_bytes, dtype=torch.uint8, device=self.device)
@@ -169,3 +185,61 @@ class _SplitFCFunction(torch.autograd.Function):
 def split_fc_softmax_ce(x_local, w_shard, labels, op: SplitFCSoftmaxCE):
     """Autograd entry: loss = SplitFC-softmax-CE(x_local, w_shard, labels); dW flows to w_shard.grad."""
     return _SplitFCFunction.apply(x_local, w_shard, labels, op)
+
+
+def symm_bytes_for(num_classes, feature_dim, world, local_batch=None, batch_counts=None, capacity=None,
+                   dtype=torch.bfloat16):
+    """Bytes of the symmetric buffer every rank needs (identical on all ranks)."""
+    counts, offs = _lib.whale_splitfc_plan(num_classes, world, capacity)
+    xdt = {torch.bfloat16: _lib.WHALE_BF16, torch.float32: _lib.WHALE_F32}[dtype]
+    B = batch_counts[0] if batch_counts is not None else local_batch
+    q, _keep = _lib.make_desc(0, world, B, feature_dim, num_classes, counts, offs, xdt, batch_counts=batch_counts)
+    return _lib.whale_splitfc_workspace_size(q)[0]
+
+
+@contextmanager
+def _env(**kv):
+    old = {k: os.environ.get(k) for k in kv}
+    os.environ.update({k: str(v) for k, v in kv.items()})
+    try:
+        yield
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def emulated_ranks(num_classes, feature_dim, world, local_batch=None, batch_counts=None, capacity=None,
+                   dtype=torch.bfloat16, device=None, spare_sms: int = 16, timeout_ms: int = 20000):
+    """N ranks of the split FC on ONE device -> ([SplitFCSoftmaxCE] * world, [stream] * world).
+
+    Test harness for the multi-rank protocol on a single GPU.  Every rank gets its own library
+    context, workspace and stream; rank p's "symmetric buffer" is a plain allocation that every
+    rank's context writes into (the same stores the NVLink path issues to a peer's mapping).
+    The ranks' kernels wait on one another, so they must run side by side: each rank's
+    persistent grids are capped to (SMs - spare_sms) / world SMs (WHALE_SM_LIMIT_R<r>),
+    WHALE_SHARED_DEVICE=1 turns programmatic dependent launch off (no kernel waits resident
+    ahead of its turn) and bounds the exchange kernels' grids, and every peer wait gives up
+    after `timeout_ms` with WHALE_ERR_COMM instead of hanging.  Issue each rank's calls on
+    its own stream (forward of every rank, then backward of every rank).
+    """
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    per = max(2, (sms - spare_sms) // world) & ~1  # even: whole 2-CTA clusters
+    if batch_counts is not None:
+        batch_counts = [int(b) for b in batch_counts]
+    nb = symm_bytes_for(num_classes, feature_dim, world, local_batch, batch_counts, capacity, dtype)
+    bufs = [torch.zeros(max(nb, 256), dtype=torch.uint8, device=device) for _ in range(world)]
+    env = {f"WHALE_SM_LIMIT_R{r}": per for r in range(world)}
+    env.update(WHALE_SHARED_DEVICE=1, WHALE_TIMEOUT_MS=int(timeout_ms))
+    ops = []
+    with _env(**env):
+        for r in range(world):
+            B = batch_counts[r] if batch_counts is not None else local_batch
+            ops.append(SplitFCSoftmaxCE(num_classes, feature_dim, B, capacity=capacity, dtype=dtype, device=device,
+                                        batch_counts=batch_counts, emulated=(r, world, bufs)))
+    torch.cuda.synchronize(device)
+    streams = [torch.cuda.Stream(device=device) for _ in range(world)]
+    return ops, streams

@@ -26,52 +26,58 @@ def fro(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf16", seed=1, steps=2, bias=False,
+def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf16", seed=1, steps=3, bias=False,
              batch=None):
+    """`steps` forward+backward steps with NEW seeded (X, y) every step (W stays), every step
+    checked against the oracle (a stale gathered row or label would show up here)."""
     bc = batch if batch is not None else [B] * world  # per-rank DP batch (NEXT-3 when uneven)
     Bt = sum(bc)
     r0 = sum(bc[:rank])
     B = bc[rank]
-    X = syn.gen_features((0, Bt), D, seed, dtype)
     W = syn.gen_weight((0, C), D, seed, regime, dtype)
-    y = syn.gen_labels((0, Bt), C, seed)
     bfull = syn.gen_bias((0, C), seed, 2.0, dtype) if bias else None
     op = SplitFCSoftmaxCE(C, D, B, capacity=capacity, dtype=syn.torch_dtype(dtype), group=dist.group.WORLD, device=dev,
                           batch_counts=batch)
     o, c = op.o_r, op.C_r
-    xr = X[r0:r0 + B].to(dev)
-    yr = y[r0:r0 + B].to(dev)
     wr = W[o:o + c].to(dev).contiguous()
     br = bfull[o:o + c].to(dev).contiguous() if bias else None
-    for _ in range(steps):  # repeated steps exercise the device epoch / flag protocol
+    ok = True
+    res = {}
+    for step in range(steps):  # repeated steps exercise the device epoch / flag protocol
+        sd = seed + 7919 * (step + 1)
+        X = syn.gen_features((0, Bt), D, sd, dtype)
+        y = syn.gen_labels((0, Bt), C, sd)
+        xr = X[r0:r0 + B].to(dev)
+        yr = y[r0:r0 + B].to(dev)
         loss = op.forward(xr, yr, wr, row_loss=True, bias=br, predictions=bias).clone()
         out = op.backward(wr, bias_grad=bias)
         dx, dw = out[0], out[1]
-    op.check()
-    torch.cuda.synchronize(dev)
-    f = oracle.forward_backward(X, W, y.numpy(), bfull)
-    losses = [torch.zeros((), device=dev) for _ in range(world)]
-    dist.all_gather(losses, loss)
-    bit_equal = all(torch.equal(l, losses[0]) for l in losses)
-    res = {
-        "B": B, "batch": bc, "D": D, "C": C, "world": world, "capacity": capacity, "regime": regime, "dtype": dtype,
-        "C_r": c, "loss": float(loss), "loss_ref": float(f["loss"]),
-        "loss_rel": abs(float(loss) - f["loss"]) / abs(f["loss"]),
-        "rowloss_rel": fro(op.row_loss.cpu(), f["row_loss"][r0:r0 + B]),
-        "dx_rel": fro(dx.float().cpu(), f["dX"][r0:r0 + B]),
-        "dw_rel": fro(dw.cpu(), f["dW"][o:o + c]),
-        "loss_bit_equal": bool(bit_equal),
-    }
-    ok = res["loss_rel"] <= 1e-3 and res["dx_rel"] <= 1e-2 and res["dw_rel"] <= 1e-2 and bit_equal
-    if bias:
-        rows = slice(r0, r0 + B)
-        Zs = np.sort(f["Z"][rows], axis=1)
-        clear = (Zs[:, -1] - Zs[:, -2]) > 1e-3
-        pred = op.pred.cpu().numpy()
-        res["db_rel"] = fro(out[2].cpu(), f["db"][o:o + c])
-        res["pred_ok"] = bool(np.array_equal(pred[clear], f["pred"][rows][clear]))
-        res["prob_rel"] = float(np.max(np.abs(op.prob.cpu().numpy() - f["prob"][rows]) / f["prob"][rows])) if B else 0.0
-        ok = ok and res["db_rel"] <= 1e-2 and res["pred_ok"] and res["prob_rel"] <= 1e-3
+        op.check()
+        torch.cuda.synchronize(dev)
+        f = oracle.forward_backward(X, W, y.numpy(), bfull)
+        losses = [torch.zeros((), device=dev) for _ in range(world)]
+        dist.all_gather(losses, loss)
+        bit_equal = all(torch.equal(l, losses[0]) for l in losses)
+        res = {
+            "B": B, "batch": bc, "D": D, "C": C, "world": world, "capacity": capacity, "regime": regime, "dtype": dtype,
+            "C_r": c, "step": step, "loss": float(loss), "loss_ref": float(f["loss"]),
+            "loss_rel": abs(float(loss) - f["loss"]) / abs(f["loss"]),
+            "rowloss_rel": fro(op.row_loss.cpu(), f["row_loss"][r0:r0 + B]),
+            "dx_rel": fro(dx.float().cpu(), f["dX"][r0:r0 + B]) if B else 0.0,
+            "dw_rel": fro(dw.cpu(), f["dW"][o:o + c]),
+            "loss_bit_equal": bool(bit_equal),
+        }
+        ok_s = res["loss_rel"] <= 1e-3 and res["dx_rel"] <= 1e-2 and res["dw_rel"] <= 1e-2 and bit_equal
+        if bias:
+            rows = slice(r0, r0 + B)
+            Zs = np.sort(f["Z"][rows], axis=1)
+            clear = (Zs[:, -1] - Zs[:, -2]) > 1e-3
+            pred = op.pred.cpu().numpy()
+            res["db_rel"] = fro(out[2].cpu(), f["db"][o:o + c])
+            res["pred_ok"] = bool(np.array_equal(pred[clear], f["pred"][rows][clear]))
+            res["prob_rel"] = float(np.max(np.abs(op.prob.cpu().numpy() - f["prob"][rows]) / f["prob"][rows])) if B else 0.0
+            ok_s = ok_s and res["db_rel"] <= 1e-2 and res["pred_ok"] and res["prob_rel"] <= 1e-3
+        ok = ok and ok_s
     res["ok"] = ok
     allres = [None] * world
     dist.all_gather_object(allres, res)

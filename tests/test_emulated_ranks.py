@@ -1,0 +1,194 @@
+"""Multi-rank parity on ONE GPU: N emulated ranks (paper_2011_09208_b200.emulated_ranks).
+
+The driver's GPU test box has one B200, so the multi-GPU protocol -- the bridge all-gather
+of X_r, y_r (A2), the per-row statistics exchange of the split softmax
+(A4, the "communication operator", PAPER.md:488 comment), the dX reduce-scatter back to the
+DP owners (A8, the bridge backward) and the uneven per-rank batch of
+the hardware-aware `replicate` (NEXT-3) -- is exercised here
+with every rank's context on cuda:0.  The ranks' "symmetric buffers" are plain device
+allocations that all contexts address directly, so the same exchange kernels issue the same
+stores and flag protocol as over NVLink; each rank runs on its own stream with its
+persistent grids capped to its share of the SMs.
+
+Every case runs >= 3 steps with DIFFERENT seeded (X, y) per step (the weights stay), each
+step checked against the fp64 oracle: loss (bit-identical on every rank), per-row loss, dX_r
+of every rank, dW_r of every shard (and db_r / predictions with a bias).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic as syn
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-3
+FRO_RTOL = 1e-2
+
+
+def _fro(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / nb) if nb > 0 else float(np.linalg.norm(a))
+
+
+@pytest.fixture(scope="module")
+def whale():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2011_09208_b200 as w
+    from paper_2011_09208_b200 import _lib
+    _lib.lib()
+    return w
+
+
+def run_emulated(whale, world, D, C, B=None, batch=None, capacity=None, regime="init", dtype="bf16", bias=False,
+                 steps=3, seed=1, expect_f1=None):
+    bc = [int(b) for b in batch] if batch is not None else [B] * world
+    Bt = sum(bc)
+    offs = np.concatenate([[0], np.cumsum(bc)]).astype(int)
+    tdt = syn.torch_dtype(dtype)
+    ops, streams = whale.emulated_ranks(C, D, world, local_batch=B, batch_counts=batch, capacity=capacity,
+                                        dtype=tdt)
+    dev = ops[0].device
+    W = syn.gen_weight((0, C), D, seed, regime, dtype)
+    bfull = syn.gen_bias((0, C), seed, 2.0, dtype) if bias else None
+    wr = [W[o.o_r:o.o_r + o.C_r].to(dev).contiguous() for o in ops]
+    br = [bfull[o.o_r:o.o_r + o.C_r].to(dev).contiguous() if bias else None for o in ops]
+    if expect_f1 is not None:
+        assert all(o.config()["f1"] == int(expect_f1) for o in ops)
+    try:
+        for step in range(steps):
+            sd = seed + 7919 * (step + 1)  # new features and labels every step
+            X = syn.gen_features((0, Bt), D, sd, dtype)
+            y = syn.gen_labels((0, Bt), C, sd)
+            keep, outs = [], []
+            for r, o in enumerate(ops):  # forward of every rank, each on its own stream
+                with torch.cuda.stream(streams[r]):
+                    xr = X[offs[r]:offs[r + 1]].to(dev)
+                    yr = y[offs[r]:offs[r + 1]].to(dev)
+                    keep.append((xr, yr))
+                    o.forward(xr, yr, wr[r], row_loss=True, bias=br[r], predictions=bias)
+            for r, o in enumerate(ops):  # then backward of every rank
+                with torch.cuda.stream(streams[r]):
+                    outs.append(o.backward(wr[r], bias_grad=bias))
+            torch.cuda.synchronize(dev)
+            for r, o in enumerate(ops):
+                with torch.cuda.stream(streams[r]):
+                    o.check()
+            f = oracle.forward_backward(X, W, y.numpy(), bfull)
+            losses = [o.loss.clone() for o in ops]
+            tag = f"world={world} step={step} D={D} C={C} batch={bc} cap={capacity} {regime} {dtype} bias={bias}"
+            assert all(torch.equal(l, losses[0]) for l in losses), (tag, [float(l) for l in losses])
+            assert abs(float(losses[0]) - f["loss"]) <= LOSS_RTOL * abs(f["loss"]), (tag, float(losses[0]), f["loss"])
+            for r, o in enumerate(ops):
+                rows = slice(offs[r], offs[r + 1])
+                cls = slice(o.o_r, o.o_r + o.C_r)
+                if bc[r]:
+                    np.testing.assert_allclose(o.row_loss.cpu().numpy(), f["row_loss"][rows],
+                                               rtol=5e-3 if dtype == "f32" else LOSS_RTOL, atol=LOSS_RTOL, err_msg=tag)
+                    assert _fro(outs[r][0].float().cpu(), f["dX"][rows]) <= FRO_RTOL, (tag, r, "dX")
+                assert _fro(outs[r][1].cpu(), f["dW"][cls]) <= FRO_RTOL, (tag, r, "dW")
+                if bias:
+                    assert _fro(outs[r][2].cpu(), f["db"][cls]) <= FRO_RTOL, (tag, r, "db")
+                    if bc[r]:
+                        Zs = np.sort(f["Z"][rows], axis=1)
+                        clear = (Zs[:, -1] - Zs[:, -2]) > (2e-2 if dtype == "f32" else 1e-3)
+                        assert np.array_equal(o.pred.cpu().numpy()[clear], f["pred"][rows][clear]), (tag, r)
+                        np.testing.assert_allclose(o.prob.cpu().numpy(), f["prob"][rows], rtol=2e-3, err_msg=tag)
+    finally:
+        for o in ops:
+            o.close()
+
+
+CASES = [
+    # world, kwargs                                               what it exercises
+    (2, dict(B=24, D=192, C=3001, regime="peaked")),              # plain path, ragged tiles
+    (2, dict(B=16, D=512, C=5000, expect_f1=True)),               # F1 (B_tot = 32), labels race check
+    (2, dict(B=16, D=1024, C=9001, regime="peaked", bias=True, expect_f1=True)),  # F1 + bias/db/pred
+    (3, dict(B=40, D=256, C=7001, regime="peaked", bias=True)),   # odd world, bias/db/predictions
+    (4, dict(B=8, D=512, C=20000, expect_f1=True)),               # F1 at N = 4
+    (4, dict(B=32, D=256, C=5000, capacity=[2, 1, 1, 1])),        # c3-like uneven class shards
+    (2, dict(B=8, D=64, C=1000, dtype="f32")),                    # tiny: fp32 operands (tf32)
+    # NEXT-3: uneven per-rank DP batch (proportional plan), a rank with no rows
+    (3, dict(batch=[30, 15, 15], D=512, C=9000)),
+    (4, dict(batch=[40, 40, 40, 0], D=256, C=3000, regime="peaked")),
+    (4, dict(batch=[12, 8, 8, 4], D=1024, C=12_011, regime="peaked", bias=True, expect_f1=True)),
+]
+
+
+@pytest.mark.parametrize("world,kw", CASES, ids=[f"n{w}-{i}" for i, (w, _) in enumerate(CASES)])
+def test_emulated_ranks_parity(whale, world, kw):
+    run_emulated(whale, world, seed=900 + world, **kw)
+
+
+def test_emulated_c2_shape(whale):
+    """c2's per-rank shape (D=2048, C=100K, B=32 per rank) at N=2 (plain path, B_tot = 64) and
+    c2's class count with B_tot = 32 (F1)."""
+    run_emulated(whale, 2, D=2048, C=100_000, B=32, steps=3, seed=9208)
+    run_emulated(whale, 2, D=2048, C=100_000, B=16, steps=3, seed=9209, expect_f1=True)
+
+
+def test_emulated_forward_only_steps(whale):
+    """Forward-only steps (eval) between training steps must not disturb the backward's
+    counters or the exchange epochs: fwd, fwd, fwd+bwd, fwd+bwd on 2 emulated ranks."""
+    world, B, D, C = 2, 24, 256, 4001
+    ops, streams = whale.emulated_ranks(C, D, world, local_batch=B)
+    dev = ops[0].device
+    W = syn.gen_weight((0, C), D, 31, "peaked", "bf16")
+    wr = [W[o.o_r:o.o_r + o.C_r].to(dev).contiguous() for o in ops]
+    try:
+        for step, do_bwd in enumerate((False, False, True, False, True)):
+            X = syn.gen_features((0, world * B), D, 40 + step, "bf16")
+            y = syn.gen_labels((0, world * B), C, 40 + step)
+            keep, outs = [], []
+            for r, o in enumerate(ops):
+                with torch.cuda.stream(streams[r]):
+                    xr, yr = X[r * B:(r + 1) * B].to(dev), y[r * B:(r + 1) * B].to(dev)
+                    keep.append((xr, yr))
+                    o.forward(xr, yr, wr[r])
+            if do_bwd:
+                for r, o in enumerate(ops):
+                    with torch.cuda.stream(streams[r]):
+                        outs.append(o.backward(wr[r]))
+            torch.cuda.synchronize(dev)
+            for o in ops:
+                o.check()
+            f = oracle.forward_backward(X, W, y.numpy())
+            assert abs(float(ops[0].loss) - f["loss"]) <= LOSS_RTOL * f["loss"], step
+            assert torch.equal(ops[0].loss, ops[1].loss)
+            if do_bwd:
+                for r, o in enumerate(ops):
+                    assert _fro(outs[r][0].float().cpu(), f["dX"][r * B:(r + 1) * B]) <= FRO_RTOL, (step, r)
+                    assert _fro(outs[r][1].cpu(), f["dW"][o.o_r:o.o_r + o.C_r]) <= FRO_RTOL, (step, r)
+    finally:
+        for o in ops:
+            o.close()
+
+
+@pytest.mark.parametrize("B,D", [(16, 512), (24, 192)])  # F1 and plain path
+def test_emulated_dead_peer_reports_comm(whale, B, D):
+    """A rank that never calls forward: the live rank's peer waits give up after the timeout,
+    its kernels finish (no trap, no sticky CUDA error) and check() reports WHALE_ERR_COMM."""
+    world, C = 2, 3000
+    ops, streams = whale.emulated_ranks(C, D, world, local_batch=B, timeout_ms=300)
+    dev = ops[0].device
+    o = ops[0]
+    X = syn.gen_features((0, B), D, 3, "bf16").to(dev)
+    y = syn.gen_labels((0, B), C, 3).to(dev)
+    W = syn.gen_weight((o.o_r, o.o_r + o.C_r), D, 3, "init", "bf16").to(dev)
+    try:
+        with torch.cuda.stream(streams[0]):
+            o.forward(X, y, W)
+            o.backward(W)
+            with pytest.raises(whale.WhaleError) as e:
+                o.check()
+        assert e.value.status == 7  # WHALE_ERR_COMM
+        torch.cuda.synchronize(dev)  # the context is healthy: no trap / sticky error
+        t = torch.ones(4, device=dev)
+        assert float(t.sum()) == 4.0
+    finally:
+        for op in ops:
+            op.close()

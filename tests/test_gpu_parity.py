@@ -233,16 +233,19 @@ def test_parity_c2_full_bench_config(whale):
         _check_full(g, oracle.forward_backward(X, W, y.numpy()), f"c2/{regime}")
 
 
+@pytest.mark.parametrize("regime", ["init", "peaked"])
 @pytest.mark.parametrize("name,B_override", [("c4", 0), ("c5", 0), ("c4", 32)])
-def test_parity_large_sampled(whale, name, B_override):
+def test_parity_large_sampled(whale, name, B_override, regime):
     """Full-size single-GPU runs of the larger configs (c4 as B_tot=256 on one GPU; c5 at
     N=1; c4's 1M classes at B_tot = 32, i.e. the F1 path over 7813 class tiles) against
-    sampled oracle rows / classes, plus the any-size property sum_j dW_j = 0."""
+    sampled oracle rows / classes, plus the any-size property sum_j dW_j = 0.  In the init
+    regime dX ~ -W_y / B_tot (the softmax part sum_j p_ij W_j is ~x/D, a few % of a row), so
+    the softmax part dX + W_y / B_tot is checked on its own as well."""
     cfg = syn.CONFIGS[name]
     seed = syn.config_seed(name, 1)
     B, D, C = B_override or cfg.B, cfg.D, cfg.C
     X = syn.gen_features((0, B), D, seed, "bf16", device="cuda")
-    W = syn.gen_weight((0, C), D, seed, "init", "bf16", device="cuda")
+    W = syn.gen_weight((0, C), D, seed, regime, "bf16", device="cuda")
     y = syn.gen_labels((0, B), C, seed, device="cuda")
     op = whale.SplitFCSoftmaxCE(C, D, B)
     loss = float(op.forward(X, y, W, row_loss=True))
@@ -255,7 +258,16 @@ def test_parity_large_sampled(whale, name, B_override):
     Xc, Wc, yc = X.cpu(), W.cpu(), y.cpu().numpy()
     s = orc.sampled_rows(Xc, Wc, yc, rows)
     np.testing.assert_allclose(row_loss[rows], s["row_loss"], rtol=LOSS_RTOL, atol=LOSS_RTOL)
-    assert _fro(dx.float().cpu().numpy()[rows], s["dX"]) <= FRO_RTOL
+    dx_rows = dx.float().cpu().numpy()[rows]
+    assert _fro(dx_rows, s["dX"]) <= FRO_RTOL
+    # the softmax part sum_j p_ij W_j / B_tot = dX + W_y / B_tot (one-hot part exact in fp64):
+    # within 1e-2 of itself, plus the floor of dX's bf16 output rounding (2^-8 of |dX|),
+    # which alone exceeds 1e-2 of the softmax part in the init regime
+    wy = orc._f64(Wc[yc[rows]]) / B
+    sm_ref = s["dX"] + wy
+    err = np.linalg.norm(dx_rows + wy - sm_ref)
+    assert err <= FRO_RTOL * np.linalg.norm(sm_ref) + 2.0 ** -8 * np.linalg.norm(s["dX"]), (
+        err, np.linalg.norm(sm_ref), np.linalg.norm(s["dX"]))
     _, _, lse = orc.row_stats_chunked(Xc, Wc)
     ref_loss = float(np.mean(lse - np.einsum("ij,ij->i", orc._f64(Xc), orc._f64(Wc[yc]))))
     assert abs(loss - ref_loss) <= LOSS_RTOL * ref_loss
@@ -298,18 +310,26 @@ def test_bias_and_predictions(whale, B, D, C, dtype):
 @pytest.mark.parametrize("B,D,C", [(32, 2048, 20_000), (64, 512, 5000)])
 def test_cuda_graph_replay(whale, B, D, C):
     """The bench captures one step as a CUDA graph and replays it: the device-resident step
-    epoch must make every replay compute the same thing as an eager step (F1 and plain path)."""
+    epoch must make every replay compute the same thing as an eager step (F1 and plain path).
+    The input CONTENTS change between replays (new features and labels copied into the
+    captured buffers), and every replay is compared bit for bit with an eager step on the same
+    inputs and with the fp64 oracle."""
     seed = 400 + B
-    X = syn.gen_features((0, B), D, seed, "bf16").cuda()
     W = syn.gen_weight((0, C), D, seed, "peaked", "bf16").cuda()
-    y = syn.gen_labels((0, B), C, seed).cuda().to(torch.int32)
+    X = torch.empty(B, D, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(B, dtype=torch.int32, device="cuda")
     op = whale.SplitFCSoftmaxCE(C, D, B)
     dx = torch.empty(B, D, dtype=torch.bfloat16, device="cuda")
     dw = torch.empty(C, D, dtype=torch.float32, device="cuda")
-    op.forward(X, y, W)
-    op.backward(W, dx, dw)
-    torch.cuda.synchronize()
-    ref = (op.loss.clone(), dx.clone(), dw.clone())
+
+    def inputs(k):
+        Xh = syn.gen_features((0, B), D, seed + 31 * k, "bf16")
+        yh = syn.gen_labels((0, B), C, seed + 31 * k)
+        return Xh, yh
+
+    Xh, yh = inputs(0)
+    X.copy_(Xh)
+    y.copy_(yh)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
@@ -320,16 +340,76 @@ def test_cuda_graph_replay(whale, B, D, C):
     with torch.cuda.graph(g):
         op.forward(X, y, W)
         op.backward(W, dx, dw)
-    for _ in range(3):
+    for k in range(1, 4):
+        Xh, yh = inputs(k)
+        X.copy_(Xh)
+        y.copy_(yh)
         dx.zero_()
         dw.zero_()
         g.replay()
         torch.cuda.synchronize()
         op.check()
-        assert torch.equal(op.loss, ref[0])
-        assert torch.equal(dx, ref[1])
-        assert torch.equal(dw, ref[2])
+        got = (op.loss.clone(), dx.clone(), dw.clone())
+        op.forward(X, y, W)  # eager step on the same inputs
+        op.backward(W, dx, dw)
+        torch.cuda.synchronize()
+        op.check()
+        assert torch.equal(got[0], op.loss), k
+        assert torch.equal(got[1], dx), k
+        assert torch.equal(got[2], dw), k
+        f = oracle.forward_backward(Xh, W.cpu(), yh.numpy())
+        assert abs(float(got[0]) - f["loss"]) <= LOSS_RTOL * f["loss"], k
+        assert _fro(got[1].float().cpu(), f["dX"]) <= FRO_RTOL, k
+        assert _fro(got[2].cpu(), f["dW"]) <= FRO_RTOL, k
     op.close()
+
+
+@pytest.mark.parametrize("B,D,C", [(32, 512, 3001), (48, 192, 3001)])  # F1 and plain path
+def test_forward_only_steps(whale, B, D, C):
+    """An eval forward (no backward) between training steps must leave the backward intact:
+    fwd, fwd, fwd+bwd, fwd, fwd+bwd with new inputs each time, all against the oracle."""
+    W = syn.gen_weight((0, C), D, 61, "peaked", "bf16")
+    wd = W.cuda()
+    op = whale.SplitFCSoftmaxCE(C, D, B)
+    for k, do_bwd in enumerate((False, False, True, False, True)):
+        X = syn.gen_features((0, B), D, 70 + k, "bf16")
+        y = syn.gen_labels((0, B), C, 70 + k)
+        xd = X.cuda()
+        loss = float(op.forward(xd, y.cuda(), wd))
+        f = oracle.forward_backward(X, W, y.numpy())
+        assert abs(loss - f["loss"]) <= LOSS_RTOL * f["loss"], k
+        if do_bwd:
+            dx, dw = op.backward(wd)
+            op.check()
+            assert _fro(dx.float().cpu(), f["dX"]) <= FRO_RTOL, k
+            assert _fro(dw.cpu(), f["dW"]) <= FRO_RTOL, k
+    op.check()
+    op.close()
+
+
+@pytest.mark.parametrize("B,D,C", [(32, 1024, 9001), (200, 520, 3001), (300, 1024, 20_000)])
+def test_gfused_backward_matches_materialised(whale, B, D, C, monkeypatch):
+    """NEXT-4b: the G-fused backward (G formed from P~ in the operand path) computes the same
+    G as the in-place rewrite (same expression), so dX / dW / db agree with the materialised
+    path to the last bit, and both match the oracle."""
+    seed = 800 + B
+    X = syn.gen_features((0, B), D, seed, "bf16")
+    W = syn.gen_weight((0, C), D, seed, "peaked", "bf16")
+    b = syn.gen_bias((0, C), seed, 2.0, "bf16")
+    y = syn.gen_labels((0, B), C, seed)
+    xd, wd, bd, yd = X.cuda(), W.cuda(), b.cuda(), y.cuda()
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("WHALE_GFUSE", mode)
+        op = whale.SplitFCSoftmaxCE(C, D, B)
+        op.forward(xd, yd, wd, bias=bd)
+        res[mode] = [t.clone() for t in op.backward(wd, bias_grad=True)]
+        op.check()
+        op.close()
+    f = oracle.forward_backward(X, W, y.numpy(), b)
+    for k, name in enumerate(("dX", "dW", "db")):
+        assert _fro(res["1"][k].float().cpu(), f[name]) <= FRO_RTOL, name
+        assert torch.equal(res["1"][k], res["0"][k]), name
 
 
 def test_random_shapes_fuzz(whale):
