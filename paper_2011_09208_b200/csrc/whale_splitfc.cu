@@ -531,6 +531,7 @@ struct whale_splitfc_ctx {
   bool pdl = true;
   bool fused_bwd = true;             // dW + dX in one persistent launch (bf16)
   bool gfuse = true;                 // G-fused backward (NEXT-4b): G formed from P~ in the bwd operand path
+  bool row_bulk = false;             // dW tiles stored as 1-D bulk row copies (bwd_sm100.cuh)
   bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
@@ -753,7 +754,13 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   if (c->fused_bwd) {
     // F1: the backward runs dW tiles only (dX came from the forward)
     c->bwd_stage_bytes = p.f1 ? p.dw.stage_bytes : std::max(p.dx.stage_bytes, p.dw.stage_bytes);
-    c->bwd_epi_bufs = env_int("WHALE_BWD_EPI", p.f1 ? 8 : 4);  // CTA-wide 16 KB store stages (dW-only: deeper)
+    // CTA-wide 16 KB store stages: dW-only (F1) deep; with dX units the load ring wants the
+    // smem (measured: 2 store stages + 4 load stages beat 4 + 3 at c4 / c5 by 7-11 %)
+    c->bwd_epi_bufs = env_int("WHALE_BWD_EPI", p.f1 ? 8 : 2);
+    // dW-only schedule (F1): row-bulk dW stores need 128 padded rows of BN fp32 of staging
+    c->row_bulk = p.f1 && env_int("WHALE_ROW_BULK", 1) != 0;
+    if (c->row_bulk)
+      c->bwd_epi_bufs = std::max(c->bwd_epi_bufs, (kBM * (p.dw.BN + 4) * 4 + 4 * kEpiBufBytes - 1) / (4 * kEpiBufBytes));
     const int fixed = 1024 + 512 + c->bwd_epi_bufs * 4 * kEpiBufBytes;
     cudaFuncAttributes fa{};
     CUDA_TRY(cudaFuncGetAttributes(&fa, splitfc_bwd_kernel<2>));  // the kernel's own __shared__ bytes
@@ -1214,6 +1221,9 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       gf.Bt = static_cast<int>(p.Bt);
       gf.inv_bt = static_cast<float>(1.0 / static_cast<double>(p.Bt));
     }
+    b.row_bulk = c->row_bulk ? 1 : 0;
+    b.dw_ptr = static_cast<float*>(dw);
+    b.dw_ld = static_cast<int>(p.D);
     b.stages = c->bwd_stages;
     b.stage_bytes = c->bwd_stage_bytes;
     b.epi_bufs = c->bwd_epi_bufs;
