@@ -103,7 +103,8 @@ whale_status_t whale_splitfc_plan_mem(int64_t num_classes, int32_t world_size, c
  *   y_r   [B]        int32        global class ids in [0, C)
  *   W_r   [C_r x D]  x_dtype      rows [o_r, o_r + C_r) of the class-major weight W
  *   dX_r  [B x D]    x_dtype      d loss / d X_r (includes the 1/B_tot of the mean)
- *   dW_r  [C_r x D]  dw_dtype     d loss / d W_r (F32 only in this version)
+ *   dW_r  [C_r x D]  dw_dtype     d loss / d W_r: WHALE_F32, or WHALE_BF16 (with bf16 operands;
+ *                                 fp32 accumulation, one RN-even rounding at the store)
  * x_dtype = WHALE_BF16 runs bf16 x bf16 -> fp32 on tcgen05 kind::f16; WHALE_F32 runs
  * fp32 storage on tcgen05 kind::tf32 (R11).
  *
@@ -194,6 +195,19 @@ whale_status_t whale_splitfc_forward_ex(whale_splitfc_ctx* ctx, const void* x_lo
  * whale_splitfc_backward(...) == whale_splitfc_backward_ex(..., NULL). */
 whale_status_t whale_splitfc_backward_ex(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
                                          void* dw_shard, float* db_shard, void* stream);
+
+/*
+ * whale_splitfc_backward_scaled -- the backward with the upstream gradient folded in (the
+ * autograd path: d(total)/d(loss) arrives as a device scalar, "utilized to
+ * compute gradients for model parameters"):
+ *   grad_scale  device float scalar g, or NULL (= 1): dX_r, dW_r and db_r are multiplied by g
+ *               inside the kernels that store them (no extra pass)
+ * The other arguments are those of whale_splitfc_backward_ex; with dw_dtype == WHALE_BF16 in the
+ * descriptor dW_r is written in bf16 (rounded once from the fp32 accumulator, after g).
+ * whale_splitfc_backward_ex(...) == whale_splitfc_backward_scaled(..., NULL, stream).
+ */
+whale_status_t whale_splitfc_backward_scaled(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
+                                             void* dw_shard, float* db_shard, const float* grad_scale, void* stream);
 
 /* Synchronise `stream` and surface device-detected errors (WHALE_ERR_LABEL, WHALE_ERR_COMM);
  * clears the error word. */

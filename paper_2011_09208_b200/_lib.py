@@ -23,7 +23,7 @@ EXPORTS = (
     "whale_splitfc_plan", "whale_splitfc_plan_mem", "whale_splitfc_workspace_size", "whale_splitfc_create", "whale_splitfc_forward",
     "whale_splitfc_backward", "whale_splitfc_check", "whale_splitfc_destroy", "whale_last_error",
     "whale_splitfc_launches_per_step", "whale_splitfc_profile_enable", "whale_splitfc_profile_read",
-    "whale_splitfc_config", "whale_splitfc_forward_ex", "whale_splitfc_backward_ex",
+    "whale_splitfc_config", "whale_splitfc_forward_ex", "whale_splitfc_backward_ex", "whale_splitfc_backward_scaled",
 )
 
 
@@ -85,6 +85,8 @@ def lib() -> ctypes.CDLL:
     L.whale_splitfc_forward_ex.restype = st
     L.whale_splitfc_backward_ex.argtypes = [vp] * 6
     L.whale_splitfc_backward_ex.restype = st
+    L.whale_splitfc_backward_scaled.argtypes = [vp] * 7
+    L.whale_splitfc_backward_scaled.restype = st
     L.whale_splitfc_check.argtypes = [vp, vp]
     L.whale_splitfc_check.restype = st
     L.whale_splitfc_destroy.argtypes = [vp]
@@ -143,7 +145,7 @@ def whale_splitfc_plan_mem(num_classes: int, world_size: int, capacity=None, mem
 
 
 def make_desc(rank, world, B, D, C, counts, offsets, x_dtype=WHALE_BF16, peer_ptrs=None, symm_bytes=0,
-              workspace_ptr=0, workspace_bytes=0, batch_counts=None):
+              workspace_ptr=0, workspace_bytes=0, batch_counts=None, dw_dtype=WHALE_F32):
     """Build a Desc; the returned tuple keeps the ctypes arrays alive.  batch_counts: optional
     per-rank DP batch [world] (NEXT-3); B must then be batch_counts[rank]."""
     c_counts = (ctypes.c_int64 * world)(*counts)
@@ -152,7 +154,7 @@ def make_desc(rank, world, B, D, C, counts, offsets, x_dtype=WHALE_BF16, peer_pt
     if peer_ptrs is not None:
         c_peers = (ctypes.c_void_p * world)(*peer_ptrs)
     c_batch = (ctypes.c_int64 * world)(*batch_counts) if batch_counts is not None else None
-    d = Desc(rank, world, B, D, C, c_counts, c_offs, x_dtype, WHALE_F32,
+    d = Desc(rank, world, B, D, C, c_counts, c_offs, x_dtype, dw_dtype,
              ctypes.cast(c_peers, ctypes.POINTER(ctypes.c_void_p)) if c_peers is not None else None,
              symm_bytes, workspace_ptr or None, workspace_bytes, c_batch)
     return d, (c_counts, c_offs, c_peers, c_batch)
@@ -188,6 +190,11 @@ def whale_splitfc_forward_ex(ctx, x_local, labels_local, w_shard, bias, loss, ro
 def whale_splitfc_backward_ex(ctx, w_shard, dx_local, dw_shard, db_shard, stream):
     _check(lib().whale_splitfc_backward_ex(ctx, w_shard, dx_local, dw_shard, db_shard or None, stream or None),
            "whale_splitfc_backward_ex")
+
+
+def whale_splitfc_backward_scaled(ctx, w_shard, dx_local, dw_shard, db_shard, grad_scale, stream):
+    _check(lib().whale_splitfc_backward_scaled(ctx, w_shard, dx_local, dw_shard, db_shard or None, grad_scale or None,
+                                               stream or None), "whale_splitfc_backward_scaled")
 
 
 def whale_splitfc_check(ctx, stream):

@@ -45,6 +45,7 @@ struct CombineArgs {
   PeerPtrs recv;        // N > 1: owners' fp32 slabs [world][B_max x D]
   int row_off[kMaxRanks + 1];
   int rank, world, Bslab;
+  const float* grad_scale;  // grad_output factor (device scalar) or NULL
 };
 
 // G-fused operand path: A stages hold P~; G[i, j] = P~[i, j] gscale[i, j / fwd_bn] - [j == y_i - o_r] / B_tot
@@ -71,8 +72,9 @@ struct BwdArgs {
   // with ONE 1-D bulk copy (cp.async.bulk) -- row-contiguous 1 KB writes instead of 128 x
   // 128 B tensor-store rows (measured 6.2 vs 5.8 TB/s, scripts/micro/bulk1d_store.cu).
   int row_bulk;         // 1: dW tiles use row-bulk stores (epi_bufs x 16 KB >= 128 x (BN + 4) x 4 B)
-  float* dw_ptr;        // dW_r [C_r x D] fp32 (row-bulk stores)
+  void* dw_ptr;         // dW_r [C_r x D] fp32 or bf16 (row-bulk stores)
   int dw_ld;            // D
+  int dw_bf16;          // 1: dW_r is stored in bf16 (RN-even from the fp32 accumulator)
 };
 
 constexpr int kBwdThreads = 384;  // 12 warps (8..11: G-fused operand transformers)
@@ -149,10 +151,11 @@ __device__ __forceinline__ void combine_unit(const CombineArgs& c, int u, float*
       acc.z -= w23.x;
       acc.w -= w23.y;
     }
-    acc.x *= c.inv_bt;
-    acc.y *= c.inv_bt;
-    acc.z *= c.inv_bt;
-    acc.w *= c.inv_bt;
+    const float f = c.inv_bt * grad_factor(c.grad_scale);
+    acc.x *= f;
+    acc.y *= f;
+    acc.z *= f;
+    acc.w *= f;
     if (c.world == 1) {
       uint2 o;
       o.x = pack_bf16x2(acc.x, acc.y);
@@ -382,9 +385,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * kMaxBN + (static_cast<uint32_t>(q * 32) << 16);
+      const float dws = is_dx ? 1.f : grad_factor(a.dx.grad_scale);  // dW carries grad_output
       if (!is_dx && a.row_bulk) {
         // ---- row-bulk dW store: this thread's row, all BN columns, one bulk copy
-        float* srow = reinterpret_cast<float*>(epi_smem) + (q * 32 + lane) * (g.BN + 4);
+        const int eb = a.dw_bf16 ? 2 : 4;
+        uint8_t* srow = epi_smem + (q * 32 + lane) * (g.BN * eb + 16);
         bulk_wait_read<0>();  // my previous row copy has left the staging row
         for (int c0 = 0; c0 < g.BN; c0 += 32) {
           uint32_t v[32];
@@ -394,16 +399,67 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
           }
+          if (a.dx.grad_scale) scale32(v, dws);
+          if (a.dw_bf16) {
 #pragma unroll
-          for (int ch = 0; ch < 8; ++ch)
-            *reinterpret_cast<uint4*>(srow + c0 + 4 * ch) = make_uint4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+            for (int ch = 0; ch < 4; ++ch)
+              *reinterpret_cast<uint4*>(srow + (c0 + 8 * ch) * 2) =
+                  make_uint4(pack_bf16x2(__uint_as_float(v[8 * ch]), __uint_as_float(v[8 * ch + 1])),
+                             pack_bf16x2(__uint_as_float(v[8 * ch + 2]), __uint_as_float(v[8 * ch + 3])),
+                             pack_bf16x2(__uint_as_float(v[8 * ch + 4]), __uint_as_float(v[8 * ch + 5])),
+                             pack_bf16x2(__uint_as_float(v[8 * ch + 6]), __uint_as_float(v[8 * ch + 7])));
+          } else {
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch)
+              *reinterpret_cast<uint4*>(srow + (c0 + 4 * ch) * 4) =
+                  make_uint4(v[4 * ch], v[4 * ch + 1], v[4 * ch + 2], v[4 * ch + 3]);
+          }
         }
         fence_proxy_async_smem();
         const int row = mb * kBM + q * 32 + lane;
         const int ncol = min(g.BN, g.N - nb * g.BN);
         if (row < g.M && ncol > 0) {
-          bulk_store_1d(a.dw_ptr + static_cast<size_t>(row) * a.dw_ld + static_cast<size_t>(nb) * g.BN, srow, ncol * 4);
+          bulk_store_1d(static_cast<uint8_t*>(a.dw_ptr) + (static_cast<size_t>(row) * a.dw_ld + static_cast<size_t>(nb) * g.BN) * eb,
+                        srow, ncol * eb);
           bulk_commit();
+        }
+        continue;
+      }
+      if (!is_dx && a.dw_bf16) {
+        // ---- bf16 dW through the tensor-store path: 64 columns (128 B) per 16 KB stage
+        for (int c0 = 0; c0 < g.BN; c0 += 64) {
+          uint32_t v[32], w[32];
+          tmem_ld32(tbase + c0, v);
+          if (c0 + 32 < g.BN) tmem_ld32(tbase + c0 + 32, w);
+          tmem_ld_wait();
+          if (c0 + 64 >= g.BN) {
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+          }
+          if (c0 + 32 >= g.BN) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) w[k] = 0u;
+          }
+          uint32_t pk[32];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            pk[k] = pack_bf16x2(__uint_as_float(v[2 * k]) * dws, __uint_as_float(v[2 * k + 1]) * dws);
+            pk[16 + k] = pack_bf16x2(__uint_as_float(w[2 * k]) * dws, __uint_as_float(w[2 * k + 1]) * dws);
+          }
+          if (threadIdx.x == 128) bulk_wait_read_n(nbuf);
+          named_bar_sync(1, 128);
+          uint8_t* b = epi_smem + buf * 4 * kEpiBufBytes + (q * 32 + lane) * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            *reinterpret_cast<uint4*>(b + ((ch ^ (lane & 7)) << 4)) =
+                make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+          fence_proxy_async_smem();
+          named_bar_sync(1, 128);
+          if (threadIdx.x == 128) {
+            tma_store_3d(&tmDW, epi_smem + buf * 4 * kEpiBufBytes, nb * g.BN + c0, mb * kBM, 0);
+            bulk_commit();
+          }
+          if (++buf == nbuf) buf = 0;
         }
         continue;
       }
@@ -415,6 +471,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
         }
+        if (!is_dx && a.dx.grad_scale) scale32(v, dws);
         if (threadIdx.x == 128) bulk_wait_read_n(nbuf);
         named_bar_sync(1, 128);
         uint8_t* b = epi_smem + buf * 4 * kEpiBufBytes + (q * 32 + lane) * 128;

@@ -592,7 +592,8 @@ __global__ void __launch_bounds__(256) dx_combine_kernel(const float* __restrict
                                                          int ncl, int Bt, int D, const float* __restrict__ lse,
                                                          const int32_t* __restrict__ y, long long o_r, long long C_r,
                                                          const void* __restrict__ w, float inv_bt, void* dx_out,
-                                                         PeerPtrs recv, RowSplit rows, int rank, int world, int Bslab) {
+                                                         PeerPtrs recv, RowSplit rows, int rank, int world, int Bslab,
+                                                         const float* grad_scale) {
   // block = 8 cluster groups x 32 float4 columns of one row b; group g sums clusters
   // g, g + 8, ... and the 8 group sums are added in group order (deterministic)
   constexpr int kG = 8, kCols = 32;
@@ -640,10 +641,11 @@ __global__ void __launch_bounds__(256) dx_combine_kernel(const float* __restrict
       acc.z -= w23.x;
       acc.w -= w23.y;
     }
-    acc.x *= inv_bt;
-    acc.y *= inv_bt;
-    acc.z *= inv_bt;
-    acc.w *= inv_bt;
+    const float f = inv_bt * (grad_scale ? __ldg(grad_scale) : 1.f);
+    acc.x *= f;
+    acc.y *= f;
+    acc.z *= f;
+    acc.w *= f;
     if (world == 1) {
       uint2 o;
       o.x = pack_bf16x2(acc.x, acc.y);

@@ -94,7 +94,17 @@ struct GemmArgs {
   int debug;                // timing experiments only: bit0 skip stores, bit1 skip TMEM loads
   float* st_out;            // store_mode 2: output base ([splits x] M x N fp32)
   int* err;
+  // d loss / d (mean loss) as a device scalar (the autograd grad_output), or NULL (= 1):
+  // multiplied into the stored outputs (plain store epilogue) / the split-K fixup result
+  const float* grad_scale;
 };
+
+// The backward's output factor: *grad_scale, or 1 without one.
+__device__ __forceinline__ float grad_factor(const float* grad_scale) { return grad_scale ? __ldg(grad_scale) : 1.f; }
+__device__ __forceinline__ void scale32(uint32_t (&v)[32], float s) {
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) * s);
+}
 
 __host__ __device__ inline int gemm_smem_bytes(int stages, int stage_bytes, int epi_bufs) {
   return 1024 /*align slack*/ + stages * stage_bytes + 4 * epi_bufs * kEpiBufBytes + 256 /*barriers*/;
@@ -172,6 +182,7 @@ __device__ __forceinline__ void fixup_share(const GemmArgs& a, int mb, int nb, i
   const int per = (total + a.splits - 1) / a.splits;
   const int e0 = sp * per, e1 = min(total, e0 + per);
   const size_t split_stride = static_cast<size_t>(a.M) * a.N;
+  const float gs = grad_factor(a.grad_scale);
   for (int e = e0 + tid; e < e1; e += 128) {
     const int r = r0 + e / nc4;
     const int c = c0 + (e % nc4) * 4;
@@ -183,6 +194,12 @@ __device__ __forceinline__ void fixup_share(const GemmArgs& a, int mb, int nb, i
       acc.y += v.y;
       acc.z += v.z;
       acc.w += v.w;
+    }
+    if (a.grad_scale) {
+      acc.x *= gs;
+      acc.y *= gs;
+      acc.z *= gs;
+      acc.w *= gs;
     }
     if (a.fix_mode == FIX_LOCAL) {
       if constexpr (ES == 2) {
@@ -414,6 +431,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row0 = mb * kBM + q * 32;  // first output row of this warp
       const int row = row0 + lane;
       if constexpr (EPI == EPI_STORE_F32) {
+        // plain stores (dW) carry the grad_output factor; split-K partials get it in the fixup
+        const bool do_scale = a.grad_scale != nullptr && a.fix_mode == FIX_NONE;
+        const float gsc = do_scale ? grad_factor(a.grad_scale) : 1.f;
         if (a.store_mode == 1) {
           // CTA-wide 128-row box: all 4 warps fill one 16 KB stage, one thread stores it
           for (int c0 = 0; c0 < a.BN; c0 += 32) {
@@ -425,6 +445,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int k = 0; k < 32; ++k) v[k] = k;
             }
+            if (do_scale) scale32(v, gsc);
             if (c0 + 32 >= a.BN) {
               tc_fence_before();
               mbar_arrive(&tempty[acc]);
@@ -457,6 +478,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               tc_fence_before();
               mbar_arrive(&tempty[acc]);
             }
+            if (do_scale) scale32(v, gsc);
             const int col = nb * a.BN + c0;
             if (rv) {
 #pragma unroll
@@ -476,6 +498,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               tc_fence_before();
               mbar_arrive(&tempty[acc]);
             }
+            if (do_scale) scale32(v, gsc);
             if (lane == 0) bulk_wait_read_n(nbuf);  // the store that last used this buffer has read it
             __syncwarp();
             uint8_t* b = ebuf + buf * kEpiBufBytes + lane * 128;

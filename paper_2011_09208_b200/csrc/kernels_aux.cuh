@@ -520,14 +520,16 @@ __global__ void __launch_bounds__(128) bias_grad_part_kernel(const void* G, long
   for (int k = 0; k < V; ++k)
     if (j0 + k < C_r) o[k] = acc[k];
 }
-__global__ void __launch_bounds__(256) bias_grad_sum_kernel(const float* part, int chunks, long long C_r, float* db) {
+__global__ void __launch_bounds__(256) bias_grad_sum_kernel(const float* part, int chunks, long long C_r, float* db,
+                                                            const float* grad_scale) {
   pdl_wait();
   pdl_trigger();
+  const float gs = grad_scale ? __ldg(grad_scale) : 1.f;
   for (long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; j < C_r;
        j += static_cast<long long>(gridDim.x) * blockDim.x) {
     float s = 0.f;
     for (int c = 0; c < chunks; ++c) s += part[c * C_r + j];
-    db[j] = s;
+    db[j] = grad_scale ? s * gs : s;
   }
 }
 

@@ -202,6 +202,7 @@ enum CounterIdx { CNT_GATHER = 0, CNT_STATS = 1, CNT_DONE = 2, CNT_SCHED = 3, CN
 
 struct Plan {
   int rank = 0, world = 1, es = 2;
+  bool dw_bf16 = false;  // dW_r stored in bf16 (fused backward only)
   int64_t B = 0, Bt = 0, D = 0, C = 0, Cr = 0, o_r = 0, ldp = 0;
   int64_t Bmax = 0;                  // largest per-rank batch (dX receive slab rows)
   int64_t Boff[kMaxRanks + 1] = {};  // rank r's rows: [Boff[r], Boff[r+1]) of the gathered batch
@@ -309,7 +310,8 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
     return fail(WHALE_ERR_INVALID_ARG, "B >= 0, D >= 1 and C >= 1 required");
   if (d->feature_dim % 8 != 0) return fail(WHALE_ERR_UNSUPPORTED, "feature_dim %% 8 != 0 (TMA 16-byte rows)");
   if (d->x_dtype != WHALE_BF16 && d->x_dtype != WHALE_F32) return fail(WHALE_ERR_UNSUPPORTED, "x_dtype");
-  if (d->dw_dtype != WHALE_F32) return fail(WHALE_ERR_UNSUPPORTED, "dw_dtype must be WHALE_F32");
+  if (d->dw_dtype != WHALE_F32 && !(d->dw_dtype == WHALE_BF16 && d->x_dtype == WHALE_BF16))
+    return fail(WHALE_ERR_UNSUPPORTED, "dw_dtype must be WHALE_F32 (or WHALE_BF16 with bf16 operands)");
   if (!d->shard_counts || !d->shard_offsets) return fail(WHALE_ERR_INVALID_ARG, "NULL shard plan");
   int64_t off = 0;
   for (int r = 0; r < d->world_size; ++r) {
@@ -321,6 +323,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   p.rank = d->rank;
   p.world = d->world_size;
   p.es = d->x_dtype == WHALE_BF16 ? 2 : 4;
+  p.dw_bf16 = d->dw_dtype == WHALE_BF16;
   p.B = d->local_batch;
   p.Boff[0] = 0;
   for (int r = 0; r < p.world; ++r) {
@@ -493,12 +496,14 @@ static int g_store_mode = [] {
   return e ? atoi(e) : 1;
 }();
 
-// fp32 output map {N, rows, splits}; box rows = 128 for the CTA-wide store (mode 1), else 32.
-static whale_status_t map3d_f32(CUtensorMap* m, const void* base, uint64_t n, uint64_t rows, uint64_t splits) {
+// fp32 (or bf16) output map {N, rows, splits}; box {128 B of columns, 128 rows for the
+// CTA-wide store (mode 1) else 32, 1}.
+static whale_status_t map3d_out(CUtensorMap* m, const void* base, uint64_t n, uint64_t rows, uint64_t splits,
+                                int es = 4) {
   const uint64_t dims[3] = {n, rows, splits};
-  const uint64_t strides[2] = {n * 4, n * rows * 4};
-  const uint32_t box[3] = {32, g_store_mode == 1 ? 128u : 32u, 1};
-  return make_map(m, base, 4, 3, dims, strides, box);
+  const uint64_t strides[2] = {n * es, n * rows * es};
+  const uint32_t box[3] = {static_cast<uint32_t>(kRowBytes / es), g_store_mode == 1 ? 128u : 32u, 1};
+  return make_map(m, base, es, 3, dims, strides, box);
 }
 
 // ============================================================================ context
@@ -751,6 +756,10 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   }
   c->fused_bwd = p.es == 2 && env_int("WHALE_FUSED_BWD", 1) != 0 && g_store_mode == 1;
   c->gfuse = c->fused_bwd && env_int("WHALE_GFUSE", 0) != 0;
+  if (p.dw_bf16 && !c->fused_bwd) {
+    delete c;
+    return fail(WHALE_ERR_UNSUPPORTED, "bf16 dW needs the fused backward (WHALE_FUSED_BWD / WHALE_STORE_MODE overrides)");
+  }
   if (c->fused_bwd) {
     // F1: the backward runs dW tiles only (dX came from the forward)
     c->bwd_stage_bytes = p.f1 ? p.dw.stage_bytes : std::max(p.dx.stage_bytes, p.dw.stage_bytes);
@@ -816,7 +825,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   if (p.f1) MAP_TRY(map2d(&c->tmP_f1, P, es, p.Cr, p.Bt, p.ldp * es, 64, kF1NB));
   MAP_TRY(map2d(&c->tmG_dx, P, es, p.Cr, p.Bt, p.ldp * es, kbk, kBM));
   MAP_TRY(map2d(&c->tmG_dw, P, es, p.Cr, p.Bt, p.ldp * es, atom, p.dw.bk));
-  MAP_TRY(map3d_f32(&c->tmDxPart, c->ws + p.L.dxpart, p.D, p.Bt, p.dx.splits));
+  MAP_TRY(map3d_out(&c->tmDxPart, c->ws + p.L.dxpart, p.D, p.Bt, p.dx.splits));
   if (es == 4) {
     const int64_t ldb = p.L.ld_bt;
     MAP_TRY(map2d(&c->tmGT, c->ws + p.L.GT, 4, p.Bt, p.Cr, ldb * 4, kbk, kBM));
@@ -1094,7 +1103,7 @@ extern "C" whale_status_t whale_splitfc_forward_ex(whale_splitfc_ctx* ctx, const
 // ============================================================================ backward
 template <int ES>
 static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* dx_local, void* dw, float* db,
-                                    cudaStream_t s) {
+                                    const float* grad_scale, cudaStream_t s) {
   const Plan& p = c->p;
   const Layout& L = p.L;
   unsigned* counters = wsp<unsigned>(c, L.counters);
@@ -1106,7 +1115,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     if (st != WHALE_OK) return st;
   }
   if (dw != c->dw_cached) {
-    whale_status_t st = map3d_f32(&c->tmDW, dw, p.D, p.Cr, 1);
+    whale_status_t st = map3d_out(&c->tmDW, dw, p.D, p.Cr, 1, p.dw_bf16 ? 2 : 4);
     if (st != WHALE_OK) return st;
     c->dw_cached = dw;
   }
@@ -1131,11 +1140,12 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
                      static_cast<long long>(p.Cr), part, fz)));
     PROFILED(K_DB, s,
              (launch(c, bias_grad_sum_kernel, dim3(std::max(1, std::min(cdiv(p.Cr, 256), 4 * p.sms))), dim3(256), 0,
-                     s, static_cast<const float*>(part), chunks, static_cast<long long>(p.Cr), db)));
+                     s, static_cast<const float*>(part), chunks, static_cast<long long>(p.Cr), db, grad_scale)));
   }
   // ---- A8 args: fused split-K fixup; N = 1 writes dX, N > 1 pushes rows to their owners
   GemmArgs ax = base_args(p.dx, static_cast<int>(p.Bt), static_cast<int>(p.D));
   ax.err = err;
+  ax.grad_scale = grad_scale;
   ax.part = wsp<float>(c, L.dxpart);
   ax.st_out = wsp<float>(c, L.dxpart);
   ax.tile_cnt = wsp<uint32_t>(c, L.tile_cnt);
@@ -1172,7 +1182,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
                      static_cast<int>(p.D), static_cast<const float*>(wsp<float>(c, L.lse)), yg,
                      static_cast<long long>(p.o_r), static_cast<long long>(p.Cr), w,
                      static_cast<float>(1.0 / static_cast<double>(p.Bt)), dx_local, recv, rs, p.rank, p.world,
-                     static_cast<int>(p.Bmax))));
+                     static_cast<int>(p.Bmax), grad_scale)));
   }
   if (ES == 2 && c->fused_bwd) {
     // ---- A7 + A8 in one persistent launch: dX units first (one per CTA), then dW tiles
@@ -1208,6 +1218,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       cb.rank = p.rank;
       cb.world = p.world;
       cb.Bslab = static_cast<int>(p.Bmax);
+      cb.grad_scale = grad_scale;
       b.tc = static_cast<int>(p.Bt) * cb.parts;
     }
     if (c->gfuse) {  // NEXT-4b: the transformer warps turn each P~ operand stage into G
@@ -1222,7 +1233,8 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       gf.inv_bt = static_cast<float>(1.0 / static_cast<double>(p.Bt));
     }
     b.row_bulk = c->row_bulk ? 1 : 0;
-    b.dw_ptr = static_cast<float*>(dw);
+    b.dw_bf16 = p.dw_bf16 ? 1 : 0;
+    b.dw_ptr = dw;
     b.dw_ld = static_cast<int>(p.D);
     b.stages = c->bwd_stages;
     b.stage_bytes = c->bwd_stage_bytes;
@@ -1244,6 +1256,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
       a.dev_epoch = dev_epoch;
       a.err = err;
+      a.grad_scale = grad_scale;
       a.st_out = static_cast<float*>(dw);
       if (p.f1) {
         a.bump_epoch = 1;
@@ -1274,6 +1287,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       GemmArgs a = base_args(p.dw, static_cast<int>(p.Cr), static_cast<int>(p.D));
       a.dev_epoch = dev_epoch;
       a.err = err;
+      a.grad_scale = grad_scale;
       a.st_out = static_cast<float*>(dw);
       PROFILED(K_DW, s, (launch_gemm<EPI_STORE_F32, false, false, 4>(c, 4, p.dw, c->tmGT, c->tmXT, c->tmDW, a, s)));
     }
@@ -1302,14 +1316,20 @@ extern "C" whale_status_t whale_splitfc_backward(whale_splitfc_ctx* ctx, const v
 
 extern "C" whale_status_t whale_splitfc_backward_ex(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
                                                     void* dw_shard, float* db_shard, void* stream) {
+  return whale_splitfc_backward_scaled(ctx, w_shard, dx_local, dw_shard, db_shard, nullptr, stream);
+}
+
+extern "C" whale_status_t whale_splitfc_backward_scaled(whale_splitfc_ctx* ctx, const void* w_shard, void* dx_local,
+                                                        void* dw_shard, float* db_shard, const float* grad_scale,
+                                                        void* stream) {
   if (!ctx || !w_shard || !dw_shard) return fail(WHALE_ERR_INVALID_ARG, "NULL argument");
   if (ctx->p.B > 0 && !dx_local) return fail(WHALE_ERR_INVALID_ARG, "NULL dx_local");
   if (!ctx->have_fwd) return fail(WHALE_ERR_STATE, "backward called before forward");
   if (reinterpret_cast<uintptr_t>(dx_local) % 16 || reinterpret_cast<uintptr_t>(dw_shard) % 16)
     return fail(WHALE_ERR_INVALID_ARG, "dx_local / dw_shard must be 16-byte aligned");
   auto s = static_cast<cudaStream_t>(stream);
-  whale_status_t st = ctx->p.es == 2 ? backward_impl<2>(ctx, w_shard, dx_local, dw_shard, db_shard, s)
-                                     : backward_impl<4>(ctx, w_shard, dx_local, dw_shard, db_shard, s);
+  whale_status_t st = ctx->p.es == 2 ? backward_impl<2>(ctx, w_shard, dx_local, dw_shard, db_shard, grad_scale, s)
+                                     : backward_impl<4>(ctx, w_shard, dx_local, dw_shard, db_shard, grad_scale, s);
   if (st == WHALE_OK) ctx->have_fwd = false;
   return st;
 }

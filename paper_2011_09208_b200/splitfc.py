@@ -30,14 +30,19 @@ class SplitFCSoftmaxCE:
         batch_counts: optional per-rank DP batch [world] (hardware-aware ``replicate``, NEXT-3;
             e.g. ``whale_splitfc_plan(B_tot, world, capacity)``); rank r's rows follow ranks < r.
         dtype: torch.bfloat16 (tcgen05 kind::f16) or torch.float32 (kind::tf32).
+        dw_dtype: dtype of the dW_r the backward writes: torch.float32 (default) or, with bf16
+            operands, torch.bfloat16 (fp32 accumulation, one rounding at the store) -- what a bf16
+            weight's .grad wants, with no conversion pass.
         group: torch.distributed process group (None -> world 1).
     """
 
     def __init__(self, num_classes: int, feature_dim: int, local_batch: int, capacity=None,
                  dtype=torch.bfloat16, group=None, device=None, mem_bytes=None, bytes_per_class=None,
-                 batch_counts=None, emulated=None):
+                 batch_counts=None, emulated=None, dw_dtype=torch.float32):
         self.C, self.D, self.B = int(num_classes), int(feature_dim), int(local_batch)
         self.dtype = dtype
+        self.dw_dtype = dw_dtype
+        dwdt = {torch.float32: _lib.WHALE_F32, torch.bfloat16: _lib.WHALE_BF16}[dw_dtype]
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         if emulated is not None:  # (rank, world, [world] uint8 device buffers): see emulated_ranks
             self.rank, self.world = int(emulated[0]), int(emulated[1])
@@ -65,7 +70,7 @@ class SplitFCSoftmaxCE:
         self.C_r, self.o_r = self.counts[self.rank], self.offsets[self.rank]
         xdt = {torch.bfloat16: _lib.WHALE_BF16, torch.float32: _lib.WHALE_F32}[dtype]
         q, _keep = _lib.make_desc(self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt,
-                                  batch_counts=self.batch_counts)
+                                  batch_counts=self.batch_counts, dw_dtype=dwdt)
         symm_bytes, local_bytes = _lib.whale_splitfc_workspace_size(q)
         self.workspace = torch.empty(local_bytes, dtype=torch.uint8, device=self.device)
         peer_ptrs = None
@@ -88,7 +93,7 @@ class SplitFCSoftmaxCE:
             self._symm = (buf, hdl)
         self._desc, self._keep = _lib.make_desc(
             self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt, peer_ptrs, symm_bytes,
-            self.workspace.data_ptr(), local_bytes, self.batch_counts)
+            self.workspace.data_ptr(), local_bytes, self.batch_counts, dwdt)
         self.ctx = _lib.whale_splitfc_create(self._desc)
         self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.row_loss = torch.zeros(self.B, dtype=torch.float32, device=self.device)
@@ -97,11 +102,14 @@ class SplitFCSoftmaxCE:
 
     # ------------------------------------------------------------------ C-ABI calls
     def forward(self, x_local: torch.Tensor, labels_local: torch.Tensor, w_shard: torch.Tensor,
-                row_loss: bool = False, bias: torch.Tensor | None = None, predictions: bool = False):
+                row_loss: bool = False, bias: torch.Tensor | None = None, predictions: bool = False,
+                loss_out: torch.Tensor | None = None):
         """-> device scalar loss (mean over the global batch).  labels: int32 (int64 is cast).
 
         bias: optional [C_r] FC bias shard (same dtype as W).  predictions=True also fills
         self.pred [B] (top-1 class over all C classes) and self.prob [B] (its probability).
+        loss_out: optional fp32 scalar tensor the loss is written to (default: self.loss, reused
+        by every call).
         """
         self._check_inputs(x_local, w_shard)
         if labels_local.dtype != torch.int32:
@@ -111,25 +119,36 @@ class SplitFCSoftmaxCE:
         if bias is not None and (bias.shape != (self.C_r,) or bias.dtype != self.dtype or not bias.is_contiguous()):
             raise ValueError(f"bias must be contiguous {self.dtype} [{self.C_r}]")
         stream = torch.cuda.current_stream(self.device).cuda_stream
+        loss = self.loss if loss_out is None else loss_out
+        if loss.dtype != torch.float32 or loss.numel() != 1 or loss.device != self.device:
+            raise ValueError("loss_out must be a one-element fp32 tensor on the op's device")
         _lib.whale_splitfc_forward_ex(self.ctx, x_local.data_ptr(), self._labels.data_ptr(), w_shard.data_ptr(),
-                                      bias.data_ptr() if bias is not None else None, self.loss.data_ptr(),
+                                      bias.data_ptr() if bias is not None else None, loss.data_ptr(),
                                       self.row_loss.data_ptr() if row_loss else None,
                                       self.pred.data_ptr() if predictions else None,
                                       self.prob.data_ptr() if predictions else None, stream)
-        return self.loss
+        return loss
 
     def backward(self, w_shard: torch.Tensor, dx_local: torch.Tensor | None = None,
-                 dw_shard: torch.Tensor | None = None, db_shard: torch.Tensor | None = None, bias_grad: bool = False):
-        """-> (dX_r [B x D] in the operand dtype, dW_r [C_r x D] fp32[, db_r [C_r] fp32 if bias_grad])."""
+                 dw_shard: torch.Tensor | None = None, db_shard: torch.Tensor | None = None, bias_grad: bool = False,
+                 grad_scale: torch.Tensor | None = None):
+        """-> (dX_r [B x D] in the operand dtype, dW_r [C_r x D] in dw_dtype[, db_r [C_r] fp32 if bias_grad]).
+
+        grad_scale: optional device fp32 scalar g (d total / d loss): every output is multiplied
+        by g inside the kernels that write it (whale_splitfc_backward_scaled)."""
         if dx_local is None:
             dx_local = torch.empty(self.B, self.D, dtype=self.dtype, device=self.device)
         if dw_shard is None:
-            dw_shard = torch.empty(self.C_r, self.D, dtype=torch.float32, device=self.device)
+            dw_shard = torch.empty(self.C_r, self.D, dtype=self.dw_dtype, device=self.device)
         if bias_grad and db_shard is None:
             db_shard = torch.empty(self.C_r, dtype=torch.float32, device=self.device)
+        if grad_scale is not None and (grad_scale.dtype != torch.float32 or grad_scale.numel() != 1
+                                       or grad_scale.device != self.device):
+            raise ValueError("grad_scale must be a one-element fp32 tensor on the op's device")
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.whale_splitfc_backward_ex(self.ctx, w_shard.data_ptr(), dx_local.data_ptr(), dw_shard.data_ptr(),
-                                       db_shard.data_ptr() if db_shard is not None else None, stream)
+        _lib.whale_splitfc_backward_scaled(self.ctx, w_shard.data_ptr(), dx_local.data_ptr(), dw_shard.data_ptr(),
+                                           db_shard.data_ptr() if db_shard is not None else None,
+                                           grad_scale.data_ptr() if grad_scale is not None else None, stream)
         if db_shard is not None:
             return dx_local, dw_shard, db_shard
         return dx_local, dw_shard
@@ -172,18 +191,29 @@ class _SplitFCFunction(torch.autograd.Function):
     def forward(ctx, x_local, w_shard, labels, op):
         ctx.op = op
         ctx.save_for_backward(w_shard)
-        return op.forward(x_local, labels, w_shard).clone()
+        # a fresh output tensor per call (the library writes the loss into it: no copy kernel)
+        return op.forward(x_local, labels, w_shard, loss_out=torch.empty((), dtype=torch.float32, device=op.device))
 
     @staticmethod
     def backward(ctx, grad_loss):
         (w_shard,) = ctx.saved_tensors
-        dx, dw = ctx.op.backward(w_shard)
-        g = grad_loss.to(torch.float32)
-        return (dx * g.to(dx.dtype)), (dw * g).to(w_shard.dtype), None, None
+        op = ctx.op
+        g = grad_loss
+        if g.dtype != torch.float32 or not g.is_contiguous():
+            g = g.to(torch.float32).contiguous()
+        # the upstream gradient is multiplied in by the kernels that store dX / dW (no extra
+        # pass); dW comes out in the op's dw_dtype (create the op with dw_dtype=w.dtype)
+        dx, dw = op.backward(w_shard, grad_scale=g.reshape(1))
+        if dw.dtype != w_shard.dtype:
+            dw = dw.to(w_shard.dtype)
+        return dx, dw, None, None
 
 
 def split_fc_softmax_ce(x_local, w_shard, labels, op: SplitFCSoftmaxCE):
-    """Autograd entry: loss = SplitFC-softmax-CE(x_local, w_shard, labels); dW flows to w_shard.grad."""
+    """Autograd entry: loss = SplitFC-softmax-CE(x_local, w_shard, labels); dW flows to w_shard.grad.
+
+    The backward runs through whale_splitfc_backward_scaled: grad_output is applied inside the
+    kernels; with ``op`` built with ``dw_dtype=w_shard.dtype`` (bf16) there is no eager pass at all."""
     return _SplitFCFunction.apply(x_local, w_shard, labels, op)
 
 
@@ -212,7 +242,8 @@ def _env(**kv):
 
 
 def emulated_ranks(num_classes, feature_dim, world, local_batch=None, batch_counts=None, capacity=None,
-                   dtype=torch.bfloat16, device=None, spare_sms: int = 16, timeout_ms: int = 20000):
+                   dtype=torch.bfloat16, device=None, spare_sms: int = 16, timeout_ms: int = 20000,
+                   dw_dtype=torch.float32):
     """N ranks of the split FC on ONE device -> ([SplitFCSoftmaxCE] * world, [stream] * world).
 
     Test harness for the multi-rank protocol on a single GPU.  Every rank gets its own library
@@ -239,7 +270,7 @@ def emulated_ranks(num_classes, feature_dim, world, local_batch=None, batch_coun
         for r in range(world):
             B = batch_counts[r] if batch_counts is not None else local_batch
             ops.append(SplitFCSoftmaxCE(num_classes, feature_dim, B, capacity=capacity, dtype=dtype, device=device,
-                                        batch_counts=batch_counts, emulated=(r, world, bufs)))
+                                        batch_counts=batch_counts, emulated=(r, world, bufs), dw_dtype=dw_dtype))
     torch.cuda.synchronize(device)
     streams = [torch.cuda.Stream(device=device) for _ in range(world)]
     return ops, streams

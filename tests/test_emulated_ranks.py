@@ -124,6 +124,40 @@ def test_emulated_ranks_parity(whale, world, kw):
     run_emulated(whale, world, seed=900 + world, **kw)
 
 
+@pytest.mark.parametrize("B,D,C", [(16, 512, 5000), (24, 192, 3001)])  # F1 and plain path
+def test_emulated_grad_scale_bf16_dw(whale, B, D, C):
+    """The scaled backward with bf16 dW across 2 emulated ranks: the reduce-scattered dX and
+    every shard's dW carry g = 1.75 (dX pushes are scaled before the owner's reduce)."""
+    world = 2
+    ops_b, streams = whale.emulated_ranks(C, D, world, local_batch=B, dw_dtype=torch.bfloat16)
+    dev = ops_b[0].device
+    try:
+        W = syn.gen_weight((0, C), D, 21, "peaked", "bf16")
+        X = syn.gen_features((0, world * B), D, 22, "bf16")
+        y = syn.gen_labels((0, world * B), C, 22)
+        g = torch.tensor([1.75], device=dev)
+        keep, outs = [], []
+        for r, o in enumerate(ops_b):
+            with torch.cuda.stream(streams[r]):
+                xr, yr = X[r * B:(r + 1) * B].to(dev), y[r * B:(r + 1) * B].to(dev)
+                wr = W[o.o_r:o.o_r + o.C_r].to(dev).contiguous()
+                keep.append((xr, yr, wr))
+                o.forward(xr, yr, wr)
+        for r, o in enumerate(ops_b):
+            with torch.cuda.stream(streams[r]):
+                outs.append(o.backward(keep[r][2], grad_scale=g))
+        torch.cuda.synchronize(dev)
+        f = oracle.forward_backward(X, W, y.numpy())
+        for r, o in enumerate(ops_b):
+            o.check()
+            assert outs[r][1].dtype == torch.bfloat16
+            assert _fro(outs[r][0].float().cpu(), 1.75 * f["dX"][r * B:(r + 1) * B]) <= FRO_RTOL, r
+            assert _fro(outs[r][1].float().cpu(), 1.75 * f["dW"][o.o_r:o.o_r + o.C_r]) <= FRO_RTOL, r
+    finally:
+        for o in ops_b:
+            o.close()
+
+
 def test_emulated_c2_shape(whale):
     """c2's per-rank shape (D=2048, C=100K, B=32 per rank) at N=2 (plain path, B_tot = 64) and
     c2's class count with B_tot = 32 (F1)."""

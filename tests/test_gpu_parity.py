@@ -220,6 +220,58 @@ def test_autograd_function(whale):
     assert _fro(W.grad.float().cpu(), 2 * f["dW"]) <= FRO_RTOL
 
 
+@pytest.mark.parametrize("B,D,C", [(32, 1024, 9001), (200, 520, 3001)])  # F1 and plain path
+def test_autograd_bf16_grad_no_eager_pass(whale, B, D, C):
+    """Autograd with a bf16 weight and an op built with dw_dtype=bf16: grad_output (here 2.5)
+    is applied inside the kernels (whale_splitfc_backward_scaled) and W.grad is written in bf16
+    directly; both gradients match 2.5 x the oracle's."""
+    X = syn.gen_features((0, B), D, 13, "bf16").cuda().requires_grad_(True)
+    W = syn.gen_weight((0, C), D, 13, "peaked", "bf16").cuda().requires_grad_(True)
+    y = syn.gen_labels((0, B), C, 13).cuda()
+    op = whale.SplitFCSoftmaxCE(C, D, B, dw_dtype=torch.bfloat16)
+    loss = whale.split_fc_softmax_ce(X, W, y, op)
+    (2.5 * loss).backward()
+    f = oracle.forward_backward(X.detach().cpu(), W.detach().cpu(), y.cpu().numpy())
+    assert W.grad.dtype == torch.bfloat16
+    assert abs(loss.item() - f["loss"]) <= LOSS_RTOL * f["loss"]
+    assert _fro(X.grad.float().cpu(), 2.5 * f["dX"]) <= FRO_RTOL
+    assert _fro(W.grad.float().cpu(), 2.5 * f["dW"]) <= FRO_RTOL
+    op.close()
+
+
+@pytest.mark.parametrize("B,D,C", [(32, 2048, 20_000), (96, 512, 7001)])
+def test_grad_scale_and_bf16_dw(whale, B, D, C):
+    """whale_splitfc_backward_scaled: outputs scale with the device scalar g (fp32 dW: within
+    fp32 rounding of g x the unscaled result); bf16 dW equals the fp32 dW rounded once."""
+    X = syn.gen_features((0, B), D, 14, "bf16").cuda()
+    W = syn.gen_weight((0, C), D, 14, "peaked", "bf16").cuda()
+    b = syn.gen_bias((0, C), 14, 2.0, "bf16").cuda()
+    y = syn.gen_labels((0, B), C, 14).cuda()
+    g = torch.tensor([-0.375], device="cuda")
+    op = whale.SplitFCSoftmaxCE(C, D, B)
+    op.forward(X, y, W, bias=b)
+    dx0, dw0, db0 = [t.clone() for t in op.backward(W, bias_grad=True)]
+    op.forward(X, y, W, bias=b)
+    dx1, dw1, db1 = op.backward(W, bias_grad=True, grad_scale=g)
+    op.check()
+    torch.testing.assert_close(dw1, dw0 * g, rtol=1e-6, atol=1e-12)
+    torch.testing.assert_close(db1, db0 * g, rtol=1e-6, atol=1e-12)
+    torch.testing.assert_close(dx1.float(), (dx0.float() * g), rtol=2 ** -7, atol=1e-9)
+    op.close()
+    op = whale.SplitFCSoftmaxCE(C, D, B, dw_dtype=torch.bfloat16)
+    op.forward(X, y, W)
+    _, dwb = op.backward(W)
+    op.check()
+    assert dwb.dtype == torch.bfloat16
+    opf = whale.SplitFCSoftmaxCE(C, D, B)
+    opf.forward(X, y, W)
+    _, dwf = opf.backward(W)
+    opf.check()
+    assert torch.equal(dwb, dwf.to(torch.bfloat16))
+    op.close()
+    opf.close()
+
+
 # ------------------------------------------------------------------ full sizes
 def test_parity_c2_full_bench_config(whale):
     """configs[1] c2 at N=1 (the bench workload): B=32, D=2048, C=100K, full oracle."""
