@@ -176,7 +176,9 @@ __device__ __forceinline__ void combine_unit(const CombineArgs& c, int u, float*
 
 constexpr int kSchedSlots = 4;
 
-template <int ES>
+// DWB: dW_r stored in bf16 (a separate instantiation, so the fp32 kernel carries none of the
+// bf16 store code and keeps its register allocation)
+template <int ES, bool DWB>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     splitfc_bwd_kernel(const __grid_constant__ CUtensorMap tmGx, const __grid_constant__ CUtensorMap tmW,
                        const __grid_constant__ CUtensorMap tmPart, const __grid_constant__ CUtensorMap tmGw,
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const float dws = is_dx ? 1.f : grad_factor(a.dx.grad_scale);  // dW carries grad_output
       if (!is_dx && a.row_bulk) {
         // ---- row-bulk dW store: this thread's row, all BN columns, one bulk copy
-        const int eb = a.dw_bf16 ? 2 : 4;
+        constexpr int eb = DWB ? 2 : 4;
         uint8_t* srow = epi_smem + (q * 32 + lane) * (g.BN * eb + 16);
         bulk_wait_read<0>();  // my previous row copy has left the staging row
         for (int c0 = 0; c0 < g.BN; c0 += 32) {
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             mbar_arrive(&tempty[acc]);
           }
           if (a.dx.grad_scale) scale32(v, dws);
-          if (a.dw_bf16) {
+          if constexpr (DWB) {
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch)
               *reinterpret_cast<uint4*>(srow + (c0 + 8 * ch) * 2) =
@@ -425,7 +427,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         continue;
       }
-      if (!is_dx && a.dw_bf16) {
+      if (DWB && !is_dx) {
         // ---- bf16 dW through the tensor-store path: 64 columns (128 B) per 16 KB stage
         for (int c0 = 0; c0 < g.BN; c0 += 64) {
           uint32_t v[32], w[32];

@@ -569,9 +569,9 @@ static whale_status_t launch(whale_splitfc_ctx* c, void (*kern)(KArgs...), dim3 
 }
 
 // cudaFuncSetAttribute acts on the current device: remember per (device, kernel slot) that the
-// opt-in shared-memory limit has been raised (slots 0..7: GEMMs, 8: fused backward).
+// opt-in shared-memory limit has been raised (slots 0..7: GEMMs, 8 / 9: fused backward fp32 / bf16 dW).
 static constexpr int kMaxDevices = 64;
-static bool g_attr_done[kMaxDevices][9] = {};
+static bool g_attr_done[kMaxDevices][10] = {};
 
 template <typename K>
 static whale_status_t ensure_smem_attr(K kern, int slot) {
@@ -689,7 +689,8 @@ static whale_status_t preload_kernels() {
       reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, false, true, 2>),
       reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, false, false, 4>),
       reinterpret_cast<const void*>(splitfc_fwd_dx_kernel),
-      reinterpret_cast<const void*>(splitfc_bwd_kernel<2>),
+      reinterpret_cast<const void*>(splitfc_bwd_kernel<2, false>),
+      reinterpret_cast<const void*>(splitfc_bwd_kernel<2, true>),
       reinterpret_cast<const void*>(stats_grad_kernel<2>),
       reinterpret_cast<const void*>(stats_grad_kernel<4>),
       reinterpret_cast<const void*>(stats_grad_multi_kernel<2>),
@@ -772,7 +773,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
       c->bwd_epi_bufs = std::max(c->bwd_epi_bufs, (kBM * (p.dw.BN + 4) * 4 + 4 * kEpiBufBytes - 1) / (4 * kEpiBufBytes));
     const int fixed = 1024 + 512 + c->bwd_epi_bufs * 4 * kEpiBufBytes;
     cudaFuncAttributes fa{};
-    CUDA_TRY(cudaFuncGetAttributes(&fa, splitfc_bwd_kernel<2>));  // the kernel's own __shared__ bytes
+    CUDA_TRY(cudaFuncGetAttributes(&fa, splitfc_bwd_kernel<2, false>));  // the kernel's own __shared__ bytes
     c->bwd_stages = std::min(8, (kSmemLimit - static_cast<int>(fa.sharedSizeBytes) - fixed) / c->bwd_stage_bytes);
     c->bwd_smem = fixed + c->bwd_stages * c->bwd_stage_bytes;
     if (c->bwd_stages < 2) c->fused_bwd = false;
@@ -1241,9 +1242,9 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     b.epi_bufs = c->bwd_epi_bufs;
     b.sched_cnt = counters + CNT_SCHED;
     const int grid = std::min(b.ux + b.tw + b.tc, p.sms);
-    auto kern = splitfc_bwd_kernel<2>;
+    auto kern = p.dw_bf16 ? splitfc_bwd_kernel<2, true> : splitfc_bwd_kernel<2, false>;
     {
-      const whale_status_t st = ensure_smem_attr(kern, 8);
+      const whale_status_t st = ensure_smem_attr(kern, p.dw_bf16 ? 9 : 8);
       if (st != WHALE_OK) return st;
     }
     PROFILED(K_BWD, s,
