@@ -48,7 +48,7 @@ constexpr int kF1PBytes = 2 * kF1NB * kRowBytes;     // P~_t^T operand: 2 atoms 
 constexpr int kF1TmemCols = 512;
 constexpr int kF1G1SlotBytes = kF1StageBytes + kF1XChunkBytes;  // G1 ring slot: W chunk + X chunk
 constexpr int kF1G2SlotBytes = 2 * kF1StageBytes;                 // G2 ring slot: 128 D rows of W
-constexpr int kF1S2 = 2;                                          // G2 ring slots
+constexpr int kF1S2Max = 4;                                       // G2 ring slots (runtime: F1Args.s2)
 constexpr int kF1EpiThreads = 256;                                // 8 epilogue warps
 constexpr int kF1Threads = 128 + kF1EpiThreads;
 constexpr float kF1Tau = 8.0f;  // lazy rescale threshold, log2 units
@@ -59,6 +59,8 @@ struct F1Args {
   int C_r;                 // classes of this shard
   int num_tiles;           // ceil(C_r / 128) = T
   int stages;              // G1 ring slots
+  int s2;                  // G2 ring slots (<= kF1S2Max)
+  int split_issue;         // 1: G1 and G2 issued by two threads (warps 1 and 2)
   long long class_offset;  // o_r
   const int32_t* labels;   // [Bt] global class ids
   const void* bias;        // [C_r] bf16 or NULL
@@ -82,9 +84,8 @@ struct F1Args {
 __device__ unsigned long long g_f1_ts[64 * 16];
 __device__ unsigned long long g_f1_cta[160 * 3];  // per-CTA [entry, after prologue, end] (debug bit 0)
 
-__host__ __device__ constexpr int f1_smem_bytes(int stages, int Dq) {
-  return 1024 + stages * kF1G1SlotBytes + kF1S2 * kF1G2SlotBytes + (kF1KC - 1) * kF1SlotBytes + 2 * kF1PBytes + 256 +
-         0 * Dq;
+__host__ __device__ constexpr int f1_smem_bytes(int stages, int s2) {
+  return 1024 + stages * kF1G1SlotBytes + s2 * kF1G2SlotBytes + (kF1KC - 1) * kF1SlotBytes + 2 * kF1PBytes + 256;
 }
 
 // Warp-wide fp32 max (sm_100a redux.sync .f32), result in every lane.
@@ -125,13 +126,13 @@ __global__ void __launch_bounds__(kF1Threads, 1)
   const int S1 = a.stages;   // G1 ring: W chunk (16 KB) + X chunk (4 KB) per slot
   uint8_t* ring1 = smem;
   uint8_t* ring2 = ring1 + S1 * kF1G1SlotBytes;  // G2 ring: one 128-D block (2 W chunks) per slot
-  uint8_t* recv = ring2 + kF1S2 * kF1G2SlotBytes;
+  uint8_t* recv = ring2 + a.s2 * kF1G2SlotBytes;
   uint8_t* pbuf = recv + (kF1KC - 1) * kF1SlotBytes;  // 2 buffers
   uint64_t* full1 = reinterpret_cast<uint64_t*>(pbuf + 2 * kF1PBytes);
   uint64_t* empty1 = full1 + S1;
   uint64_t* full2 = empty1 + S1;
-  uint64_t* empty2 = full2 + kF1S2;
-  uint64_t* zfull = empty2 + kF1S2;  // 3 Z buffers
+  uint64_t* empty2 = full2 + a.s2;
+  uint64_t* zfull = empty2 + a.s2;  // 3 Z buffers
   uint64_t* zempty = zfull + 3;
   uint64_t* pfull = zempty + 3;      // 2 P~ buffers
   uint64_t* pempty = pfull + 2;      // completes when G2 of that buffer's tile finished
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
       mbar_init(&full1[i], 1);
       mbar_init(&empty1[i], 1);
     }
-    for (int i = 0; i < kF1S2; ++i) {
+    for (int i = 0; i < a.s2; ++i) {
       mbar_init(&full2[i], 1);
       mbar_init(&empty2[i], 1);
     }
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
             mbar_arrive_expect_tx(&full2[stage], 2 * kF1StageBytes);
             tma_load_2d_hint(slot, &tmW, &full2[stage], d0 + (2 * m) * 64, row0, drop);
             tma_load_2d_hint(slot + kF1StageBytes, &tmW, &full2[stage], d0 + (2 * m + 1) * 64, row0, drop);
-            if (++stage == kF1S2) {
+            if (++stage == a.s2) {
               stage = 0;
               phase ^= 1u;
             }
@@ -238,8 +239,11 @@ __global__ void __launch_bounds__(kF1Threads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ===================== MMA issuer =====================
+  } else if (warp == 1 || (warp == 2 && a.split_issue)) {
+    // ===================== MMA issuer(s) =====================
+    // split_issue: warp 1 issues G1 only and warp 2 (the TMEM allocator, idle otherwise) G2
+    // only, so a G2 block waiting on its L2 re-read never holds back the G1 stream from HBM
+    // (tcgen05.commit tracks the issuing thread's MMAs; G1 and G2 touch disjoint TMEM / smem).
     if (lane == 0) {
       const uint32_t idesc1 = umma_idesc(kF1TileC, kF1NB, false, false, 1u);
       const uint32_t idesc2 = umma_idesc(128, kF1NB, true, false, 1u);
@@ -259,11 +263,46 @@ __global__ void __launch_bounds__(kF1Threads, 1)
           umma_bf16(tmem_base + ucol0 + i * kF1NB, ad, bd, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&empty2[s2]);
-        if (++s2 == kF1S2) {
+        if (++s2 == a.s2) {
           s2 = 0;
           ph2 ^= 1u;
         }
       };
+      if (a.split_issue) {
+        if (warp == 1) {
+          for (int p = 0; p < my_tiles; ++p) {
+            if (dbg && p < 64) g_f1_ts[p * 16 + 0] = gtime_ns();
+            const int zb = p % 3;
+            mbar_wait(&zempty[zb], ((p / 3) & 1) ^ 1u);
+            tc_fence_after();
+            for (int k = 0; k < KQ; ++k) {
+              mbar_wait(&full1[s1], ph1);
+              tc_fence_after();
+              const uint32_t aS = r1 + s1 * kF1G1SlotBytes;
+              const uint32_t bS = aS + kF1StageBytes;
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                umma_bf16(tmem_base + zb * kF1NB, umma_sdesc(aS + kk * 32, 16, 1024), umma_sdesc(bS + kk * 32, 16, 1024),
+                          idesc1, (k > 0 || kk > 0) ? 1u : 0u);
+              umma_commit(&empty1[s1]);
+              if (++s1 == S1) {
+                s1 = 0;
+                ph1 ^= 1u;
+              }
+            }
+            umma_commit(&zfull[zb]);
+            if (dbg && p < 64) g_f1_ts[p * 16 + 1] = gtime_ns();
+          }
+        } else {
+          for (int j = 0; j < my_tiles; ++j) {
+            mbar_wait(&pfull[j & 1], static_cast<uint32_t>((j >> 1) & 1));  // P~_j^T in smem, U rescaled
+            tc_fence_after();
+            for (int i = 0; i < KQ / 2; ++i) g2_block(j, i);
+            umma_commit(&pempty[j & 1]);
+            if (dbg && j < 64) g_f1_ts[j * 16 + 2] = gtime_ns();
+          }
+        }
+      } else
       // Period p: G1 of tile p, with G2 of tile p - 1 interleaved (one block per G1 chunk pair)
       // as soon as that tile's epilogue has published P~, and drained at the period end -- so
       // G2 re-reads W about one period after G1 brought it into L2 (short reuse distance).

@@ -210,7 +210,7 @@ struct Plan {
   GemmCfg fwd, dw, dx;
   // F1 (fwd_dx_sm100.cuh): fused logits + dX partials, W_r read once (bf16, B_tot <= 32)
   bool f1 = false;
-  int f1_ncl = 0, f1_stages = 0, f1_smem = 0, f1_Dq = 0;
+  int f1_ncl = 0, f1_stages = 0, f1_smem = 0, f1_Dq = 0, f1_s2 = 2;
   Layout L;
 };
 
@@ -376,10 +376,11 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
       p.f1_ncl = std::min(sms / kF1KC, T);  // upper bound; create() lowers it to the co-resident count
       // stages: provisional here (host-only planning); create() sizes them with the kernel's
       // real static shared memory
-      const int fixed = f1_smem_bytes(0, p.f1_Dq) + 2048;
-      p.f1_stages = std::min(8, (kSmemLimit - fixed) / kF1G1SlotBytes);
-      p.f1_smem = f1_smem_bytes(p.f1_stages, p.f1_Dq);
-      if (p.f1_stages < 4) p.f1 = false;
+      p.f1_s2 = std::max(1, std::min(kF1S2Max, env_int("WHALE_F1_S2", 3)));
+      const int fixed = f1_smem_bytes(0, p.f1_s2) + 2048;
+      p.f1_stages = std::min(env_int("WHALE_F1_S1", 8), (kSmemLimit - fixed) / kF1G1SlotBytes);
+      p.f1_smem = f1_smem_bytes(p.f1_stages, p.f1_s2);
+      if (p.f1_stages < 3) p.f1 = false;
     }
     if (p.f1) {  // the statistics / gradient pipeline sees 128-class tiles
       p.fwd.BN = kF1TileC;
@@ -783,12 +784,12 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     // F1 clusters must all be co-resident (one wave): not every GPC holds a multiple of KC SMs
     cudaFuncAttributes fa{};
     CUDA_TRY(cudaFuncGetAttributes(&fa, splitfc_fwd_dx_kernel));
-    const int fixed = f1_smem_bytes(0, p.f1_Dq) + static_cast<int>(fa.sharedSizeBytes);
-    c->p.f1_stages = std::min(8, (kSmemLimit - fixed) / kF1G1SlotBytes);
-    c->p.f1_smem = f1_smem_bytes(c->p.f1_stages, p.f1_Dq);
-    if (c->p.f1_stages < 4) {
+    const int fixed = f1_smem_bytes(0, p.f1_s2) + static_cast<int>(fa.sharedSizeBytes);
+    c->p.f1_stages = std::min(env_int("WHALE_F1_S1", 8), (kSmemLimit - fixed) / kF1G1SlotBytes);
+    c->p.f1_smem = f1_smem_bytes(c->p.f1_stages, p.f1_s2);
+    if (c->p.f1_stages < 3) {
       delete c;
-      return fail(WHALE_ERR_UNSUPPORTED, "F1 shared memory: %d static bytes leave < 4 stages", (int)fa.sharedSizeBytes);
+      return fail(WHALE_ERR_UNSUPPORTED, "F1 shared memory: %d static bytes leave < 3 stages", (int)fa.sharedSizeBytes);
     }
     CUDA_TRY(cudaFuncSetAttribute(splitfc_fwd_dx_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kSmemLimit - static_cast<int>(fa.sharedSizeBytes)));
@@ -943,6 +944,8 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.C_r = static_cast<int>(p.Cr);
     a.num_tiles = p.fwd.n_blocks;
     a.stages = p.f1_stages;
+    a.s2 = p.f1_s2;
+    a.split_issue = env_int("WHALE_F1_SPLIT", 1);
     a.class_offset = p.o_r;
     a.labels = yg;
     a.bias = bias;
