@@ -97,6 +97,9 @@ struct GemmArgs {
   // d loss / d (mean loss) as a device scalar (the autograd grad_output), or NULL (= 1):
   // multiplied into the stored outputs (plain store epilogue) / the split-K fixup result
   const float* grad_scale;
+  // L2 policy of the B (W_r) loads: 0 normal, 1 evict_last (the logits keep a W_r shard that
+  // fits in L2 resident for the backward's dX pass, which reads it again with evict_first)
+  int b_keep_l2;
 };
 
 // The backward's output factor: *grad_scale, or 1 without one.
@@ -314,6 +317,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t l2_keep = l2_policy_evict_last();
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
       const int box_bytes = bk * kRowBytes;
       const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
@@ -347,7 +351,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tma_load_2d_mc(sB + j * box_bytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * bk, 0x3);
             }
           } else if (!B_MN) {
-            tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
+            if (a.b_keep_l2) tma_load_2d_hint(sB, &tmB, &full[stage], kb * kBK, nb * a.BN, l2_keep);
+            else tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
           } else {
             for (int j = 0; j < a.BN / kAtom; ++j)
               tma_load_2d(sB + j * box_bytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * bk);

@@ -538,6 +538,7 @@ struct whale_splitfc_ctx {
   bool fused_bwd = true;             // dW + dX in one persistent launch (bf16)
   bool gfuse = true;                 // G-fused backward (NEXT-4b): G formed from P~ in the bwd operand path
   bool row_bulk = false;             // dW tiles stored as 1-D bulk row copies (bwd_sm100.cuh)
+  bool w_l2 = false;                 // plain path: W_r kept L2-resident from the logits to the dX pass
   bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
@@ -758,6 +759,13 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   }
   c->fused_bwd = p.es == 2 && env_int("WHALE_FUSED_BWD", 1) != 0 && g_store_mode == 1;
   c->gfuse = c->fused_bwd && env_int("WHALE_GFUSE", 0) != 0;
+  {
+    // WHALE_W_L2=1: on the plain path the logits load W_r with evict_last and the backward's dX
+    // units (its second and last reader, scheduled first) with evict_first, so a shard that
+    // fits in the 126 MB L2 is read from HBM once per step.  Measured at c2 N = 4 (W_r = 102 MB):
+    // step 144 -> 164 us (the pinned lines crowd out P~ / dW traffic) -- off by default.
+    c->w_l2 = !p.f1 && c->fused_bwd && env_int("WHALE_W_L2", 0) == 1;
+  }
   if (p.dw_bf16 && !c->fused_bwd) {
     delete c;
     return fail(WHALE_ERR_UNSUPPORTED, "bf16 dW needs the fused backward (WHALE_FUSED_BWD / WHALE_STORE_MODE overrides)");
@@ -988,6 +996,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.labels = yg;
     a.bias = bias;
     a.a_tile = wsp<int32_t>(c, L.a_tile);
+    a.b_keep_l2 = c->w_l2 ? 1 : 0;
     a.class_offset = p.o_r;
     a.m_tile = wsp<float>(c, L.m_tile);
     a.s_tile = wsp<float>(c, L.s_tile);
@@ -1237,6 +1246,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       gf.inv_bt = static_cast<float>(1.0 / static_cast<double>(p.Bt));
     }
     b.row_bulk = c->row_bulk ? 1 : 0;
+    b.w_last_use = c->w_l2 ? 1 : 0;
     b.dw_bf16 = p.dw_bf16 ? 1 : 0;
     b.dw_ptr = dw;
     b.dw_ld = static_cast<int>(p.D);
