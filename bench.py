@@ -257,26 +257,10 @@ def main():
         torch.cuda.synchronize()
         total_ms = sum(a.elapsed_time(b) for a, b in evs)
     else:
-        # inputs larger than L2: no flush between steps, so the K steps run back to back as ONE
-        # graph of K steps (PDL edges between consecutive steps too: step k+1's prologue may
-        # overlap step k's tail, as in a training loop); every step still runs all its work
-        run_k = run
-        if not args.no_graph:
-            graph_k = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph_k):
-                for _ in range(args.steps):
-                    step()
-            graph_k.replay()
-            torch.cuda.synchronize()
-            op.check()
-            run_k = graph_k.replay
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
-        if run_k is run:
-            for _ in range(args.steps):
-                run()
-        else:
-            run_k()
+        for _ in range(args.steps):
+            run()
         b.record(s)
         torch.cuda.synchronize()
         total_ms = a.elapsed_time(b)
@@ -445,9 +429,7 @@ def main():
                    "dirty flush lines are written back inside a step)" if flush_l2
                    else f"inputs larger than L2 (W shard {w_bytes / 2 ** 20:.0f} MiB > 2x126 MiB)"),
             "tiles": {k: cfgj[k] for k in ("fwd", "dw", "dx")},
-            "launch": ("eager" if args.no_graph else
-                       ("CUDA graph per step (PDL edges), L2 flush between steps" if flush_l2 else
-                        "one CUDA graph of the K timed steps (PDL edges, also between steps)")),
+            "launch": "eager" if args.no_graph else "CUDA graph per step (PDL edges)",
         },
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": X.numel() * X.element_size() + y.numel() * 4,

@@ -75,8 +75,6 @@ struct BwdArgs {
   void* dw_ptr;         // dW_r [C_r x D] fp32 or bf16 (row-bulk stores)
   int dw_ld;            // D
   int dw_bf16;          // 1: dW_r is stored in bf16 (RN-even from the fp32 accumulator)
-  int w_last_use;       // 1: the dX W_r loads are W_r's last use this step (evict_first; the
-                        //    logits kept W_r L2-resident, GemmArgs.b_keep_l2)
 };
 
 constexpr int kBwdThreads = 384;  // 12 warps (8..11: G-fused operand transformers)
@@ -255,7 +253,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t tx_dw = static_cast<uint32_t>(dw_a_bytes + (W.BN / kAtom) * dw_box);
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t l2_drop = l2_policy_evict_first();
       int unit = blockIdx.x;
       for (int it = 0;; ++it) {
         const int slot = it % kSchedSlots;
@@ -276,12 +273,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             uint8_t* sB = sA + kStageABytes;
             mbar_arrive_expect_tx(&full[stage], tx_dx);
             tma_load_2d(sA, &tmGx, &full[stage], kb * kBK, mb * kBM);
-            for (int j = 0; j < X.BN / kAtom; ++j) {
-              if (a.w_last_use)
-                tma_load_2d_hint(sB + j * kBK * kRowBytes, &tmW, &full[stage], nb * X.BN + j * kAtom, kb * kBK, l2_drop);
-              else
-                tma_load_2d(sB + j * kBK * kRowBytes, &tmW, &full[stage], nb * X.BN + j * kAtom, kb * kBK);
-            }
+            for (int j = 0; j < X.BN / kAtom; ++j)
+              tma_load_2d(sB + j * kBK * kRowBytes, &tmW, &full[stage], nb * X.BN + j * kAtom, kb * kBK);
             if (++stage == a.stages) {
               stage = 0;
               phase ^= 1u;

@@ -44,6 +44,7 @@ constexpr int kBM = 128;               // MMA M (rows of A per tile)
 constexpr int kRowBytes = 128;         // one SWIZZLE_128B row: K elements per stage = 128 / ES
 constexpr int kMaxBN = 256;            // accumulator columns per TMEM buffer
 constexpr int kGemmThreads = 256;      // 8 warps
+constexpr int kStatsGemmThreads = 384; // EPI_FWD_STATS: 12 warps (warps 4..11 = 2 epilogue groups)
 constexpr int kStageABytes = kBM * kRowBytes;   // 16 KB
 constexpr int kEpiBufBytes = 4096;     // per epilogue warp per buffer: 32 rows x 128 B
 constexpr int kTmemCols = 512;
@@ -97,9 +98,6 @@ struct GemmArgs {
   // d loss / d (mean loss) as a device scalar (the autograd grad_output), or NULL (= 1):
   // multiplied into the stored outputs (plain store epilogue) / the split-K fixup result
   const float* grad_scale;
-  // L2 policy of the B (W_r) loads: 0 normal, 1 evict_last (the logits keep a W_r shard that
-  // fits in L2 resident for the backward's dX pass, which reads it again with evict_first)
-  int b_keep_l2;
 };
 
 // The backward's output factor: *grad_scale, or 1 without one.
@@ -253,9 +251,195 @@ __device__ __forceinline__ void end_of_step_ticket(const GemmArgs& a, uint32_t e
   }
 }
 
+// Split-FC forward epilogue (EPI_FWD_STATS) by warps 4..11: warp w reads TMEM lane quadrant
+// w % 4 (one thread per output row) and belongs to column group g = (w - 4) / 4, which owns the
+// tile's P~ chunks (128-byte rows: 128 / ES columns) g, g + 2, ...  Pass 1: row max over the
+// group's chunks (8 independent chains), combined through smem with the other group; pass 2:
+// P~ = exp(z - m_tile) -> bf16 / fp32 staging -> TMA store, partial sum-exp (4 chains), the
+// first column holding the max and the label logit; group 0 writes the tile statistics from
+// both groups' partials in a fixed order.  Two 256-thread named barriers per tile.
+template <int ES>
+__device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUtensorMap& tmOut, uint32_t tmem_base,
+                                                   uint8_t* epi_smem, uint64_t* tfull, uint64_t* tempty, int unit0,
+                                                   int ustride, uint32_t crank, int warp, int lane) {
+  // 1.5 KB of static smem (the GEMM's stage budget leaves ~1.7 KB): s_x[g][r] holds group g's
+  // row max after pass 1; after pass 2 group 1 puts its partial sum into s_x[0][r] (a slot only
+  // thread (1, r) reads, and already has) and its first-max column into s_arg1[r]
+  __shared__ float s_x[2][kBM];
+  __shared__ int s_arg1[kBM];
+  constexpr int kChunk = kRowBytes / ES;  // P~ columns per 128-byte smem row
+  constexpr float kLog2e = 1.4426950408889634f;
+  const int q = warp & 3;
+  const int g = (warp - 4) >> 2;
+  const int r = q * 32 + lane;  // row within the tile
+  const int nbw = a.epi_bufs / 2 > 0 ? a.epi_bufs / 2 : 1;  // staging buffers per warp
+  uint8_t* ebuf = epi_smem + (g * 4 + q) * nbw * kEpiBufBytes;
+  const bool has_bias = a.bias != nullptr;
+  int buf = 0;
+  int it = 0;
+  for (int tile = unit0; tile < a.num_tiles; tile += ustride, ++it) {
+    int mb, nb, sp, kb0, kb1;
+    decode_unit(a, tile, crank, mb, nb, sp, kb0, kb1);
+    const int acc = it & 1;
+    mbar_wait(&tfull[acc], (it >> 1) & 1);
+    tc_fence_after();
+    const uint32_t tbase = tmem_base + acc * kMaxBN + (static_cast<uint32_t>(q * 32) << 16);
+    const int row0 = mb * kBM + q * 32;
+    const int row = row0 + lane;
+    const bool rv = row < a.M;
+    const bool wv = row0 < a.M;  // warp-uniform: rows of this warp exist
+    const int ncol = min(a.BN, a.N - nb * a.BN);  // valid classes in this tile
+    const int nch = a.BN / kChunk;
+    const long long bcol0 = static_cast<long long>(nb) * a.BN;
+    auto bias_at = [&](int c) -> float {
+      if (bcol0 + c >= a.N) return 0.f;
+      if constexpr (ES == 2) return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(a.bias) + bcol0 + c));
+      else return __ldg(reinterpret_cast<const float*>(a.bias) + bcol0 + c);
+    };
+    // fast path (full tile, no bias, no top-1 wanted): ~4 instructions per logit
+    const bool want_arg = a.a_tile != nullptr;
+    const bool fast = ncol == a.BN && !has_bias && !want_arg;
+    // ---- pass 1: this group's row max
+    float mxk[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mxk[k] = -INFINITY;
+    if (wv) {
+      for (int ch = g; ch < nch; ch += 2) {
+        for (int h = 0; h < kChunk; h += 32) {
+          const int c0 = ch * kChunk + h;
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          tmem_ld_wait();
+          if (fast) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) mxk[c & 7] = fmaxf(mxk[c & 7], __uint_as_float(v[c]));
+          } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const float z = __uint_as_float(v[c]) + (has_bias ? bias_at(c0 + c) : 0.f);
+              mxk[c & 7] = fmaxf(mxk[c & 7], (c0 + c < ncol) ? z : -INFINITY);
+            }
+          }
+        }
+      }
+    }
+    const float my_mx = fmaxf(fmaxf(fmaxf(mxk[0], mxk[1]), fmaxf(mxk[2], mxk[3])),
+                              fmaxf(fmaxf(mxk[4], mxk[5]), fmaxf(mxk[6], mxk[7])));
+    s_x[g][r] = my_mx;
+    named_bar_sync(2, 256);
+    const float mx = g == 0 ? fmaxf(my_mx, s_x[1][r]) : fmaxf(s_x[0][r], my_mx);  // same order: max(g0, g1)
+    const float mxl = mx * kLog2e;
+    long long yl = -1;
+    if (rv) yl = static_cast<long long>(a.labels[row]) - a.class_offset - bcol0;
+    // ---- pass 2: P~, partial sums, first column of the max, label logit
+    float sk[4] = {0.f, 0.f, 0.f, 0.f};
+    int am = 0x7fffffff;
+    float zy = 0.f;
+    bool has_zy = false;
+    if (wv) {
+      for (int ch = g; ch < nch; ch += 2) {
+        if (lane == 0) {  // the store that last used this buffer has read it
+          if (nbw >= 4) bulk_wait_read<3>();
+          else if (nbw >= 2) bulk_wait_read<1>();
+          else bulk_wait_read<0>();
+        }
+        __syncwarp();
+        uint8_t* b = ebuf + buf * kEpiBufBytes + lane * 128;
+        for (int h = 0; h < kChunk; h += 32) {
+          const int c0 = ch * kChunk + h;
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          tmem_ld_wait();
+          uint32_t pk[32];
+          // the label logit: one select per logit, stored once per tile below
+          const long long yrel = yl - c0;
+          if (yrel >= 0 && yrel < 32 && c0 + yrel < ncol) {
+            has_zy = true;
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (c == yrel) zy = __uint_as_float(v[c]) + (has_bias ? bias_at(c0 + c) : 0.f);
+          }
+          if (fast) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+              const float p0 = ex2_approx(fmaf(__uint_as_float(v[c]), kLog2e, -mxl));
+              const float p1 = ex2_approx(fmaf(__uint_as_float(v[c + 1]), kLog2e, -mxl));
+              sk[(c >> 1) & 3] += p0 + p1;
+              if constexpr (ES == 2) {
+                pk[c >> 1] = pack_bf16x2(p0, p1);
+              } else {
+                pk[c] = __float_as_uint(p0);
+                pk[c + 1] = __float_as_uint(p1);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 32; c += 2) {
+              const float z0 = __uint_as_float(v[c]) + (has_bias ? bias_at(c0 + c) : 0.f);
+              const float z1 = __uint_as_float(v[c + 1]) + (has_bias ? bias_at(c0 + c + 1) : 0.f);
+              const bool ok0 = c0 + c < ncol, ok1 = c0 + c + 1 < ncol;
+              const float p0 = ok0 ? ex2_approx(fmaf(z0, kLog2e, -mxl)) : 0.f;
+              const float p1 = ok1 ? ex2_approx(fmaf(z1, kLog2e, -mxl)) : 0.f;
+              sk[(c >> 1) & 3] += p0 + p1;
+              if (want_arg) {
+                if (ok0 && z0 == mx) am = min(am, c0 + c);
+                if (ok1 && z1 == mx) am = min(am, c0 + c + 1);
+              }
+              if constexpr (ES == 2) {
+                pk[c >> 1] = pack_bf16x2(p0, p1);
+              } else {
+                pk[c] = __float_as_uint(p0);
+                pk[c + 1] = __float_as_uint(p1);
+              }
+            }
+          }
+          // this half-chunk's 16-byte pieces: bf16 -> 4 pieces at h / 8, fp32 -> 8 pieces
+          constexpr int kPieces = 32 * ES / 16;
+#pragma unroll
+          for (int k = 0; k < kPieces; ++k) {
+            const int pc = (h * ES) / 16 + k;  // 16-byte piece within the 128-byte row
+            *reinterpret_cast<uint4*>(b + ((pc ^ (lane & 7)) << 4)) =
+                make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmOut, ebuf + buf * kEpiBufBytes, nb * a.BN + ch * kChunk, row0);
+          bulk_commit();
+        }
+        if (++buf == nbw) buf = 0;
+      }
+    }
+    tc_fence_before();
+    mbar_arrive(&tempty[acc]);  // this thread's TMEM reads of the tile are done (256 arrivals)
+    if (has_zy) a.zy[row] = zy;
+    const float my_sum = (sk[0] + sk[1]) + (sk[2] + sk[3]);
+    if (g == 1) {
+      s_x[0][r] = my_sum;
+      s_arg1[r] = am;
+    }
+    named_bar_sync(2, 256);
+    if (g == 0 && rv) {
+      const float sum = my_sum + s_x[0][r];
+      int amin = min(am, s_arg1[r]);
+      if (amin == 0x7fffffff) amin = 0;  // no column equals the max (NaN inputs): any valid id
+      a.m_tile[static_cast<size_t>(row) * a.n_blocks + nb] = mx;
+      a.s_tile[static_cast<size_t>(row) * a.n_blocks + nb] = sum;
+      if (a.a_tile != nullptr)
+        a.a_tile[static_cast<size_t>(row) * a.n_blocks + nb] = static_cast<int32_t>(a.class_offset + bcol0 + amin);
+    }
+  }
+  if (lane == 0) bulk_wait<0>();
+}
+
 // ES = operand element size: 2 -> bf16 (kind::f16), 4 -> fp32 storage run as kind::tf32.
+// EPI_FWD_STATS runs 12 warps: its epilogue (two passes over the accumulator, an exp per
+// logit) is the slow side of the TMEM double buffer when K is short (c4: D = 512), so two
+// groups of 4 warps split each tile's column chunks (interleaved) and combine their row
+// max / sum / top-1 through shared memory.
 template <int EPI, bool A_MN, bool B_MN, int ES>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGemmThreads, 1)
     splitfc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmOut, const GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -286,7 +470,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], EPI == EPI_FWD_STATS ? 256 : 128);
     }
     fence_mbar_init();
   }
@@ -317,7 +501,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t l2_keep = l2_policy_evict_last();
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
       const int box_bytes = bk * kRowBytes;
       const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
@@ -351,8 +534,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tma_load_2d_mc(sB + j * box_bytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * bk, 0x3);
             }
           } else if (!B_MN) {
-            if (a.b_keep_l2) tma_load_2d_hint(sB, &tmB, &full[stage], kb * kBK, nb * a.BN, l2_keep);
-            else tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
+            tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
           } else {
             for (int j = 0; j < a.BN / kAtom; ++j)
               tma_load_2d(sB + j * box_bytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * bk);
@@ -411,15 +593,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
       }
     }
+  } else if (EPI == EPI_FWD_STATS && warp >= 4) {
+    // ===================== logits epilogue: 8 warps, 2 column groups =====================
+    // N > 1: the gathered labels are peer-written (bridge_gather); acquire the gather flags
+    // here too before any label read (the producer's acquire orders only its own lane)
+    if (a.wait_flags != nullptr && threadIdx.x == 128)
+      for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
+    named_bar_sync(2, 256);
+    fwd_stats_epilogue<ES>(a, tmOut, tmem_base, epi_smem, tfull, tempty, unit0, ustride, crank, warp, lane);
   } else if (warp >= 4) {
     // ===================== epilogue =====================
-    if constexpr (EPI == EPI_FWD_STATS) {
-      // N > 1: the gathered labels are peer-written (bridge_gather); acquire the gather flags
-      // here too before any label read (the producer's acquire orders only its own lane)
-      if (a.wait_flags != nullptr && threadIdx.x == 128)
-        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
-      named_bar_sync(1, 128);
-    }
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int nbuf = a.epi_bufs;
     uint8_t* ebuf = epi_smem + q * nbuf * kEpiBufBytes;
@@ -523,95 +706,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_fence_before();
           mbar_arrive(&tempty[acc]);
         }
-      } else if (row0 < a.M) {  // warp-uniform: skip warps whose rows are all padding
-        {
-          const bool rv = row < a.M;
-          const int ncol = min(a.BN, a.N - nb * a.BN);  // valid classes in this tile
-          constexpr float kLog2e = 1.4426950408889634f;
-          // pass 1: row max (and its first column = top-1 within the tile) over valid classes
-          // FC bias (NEXT-4): every lane of a warp reads the same column -> broadcast loads
-          // through L1 (no shared-memory staging, so the stage count is unchanged)
-          const bool has_bias = a.bias != nullptr;
-          const long long bcol0 = static_cast<long long>(nb) * a.BN;
-          auto bias_at = [&](int c) -> float {
-            if (bcol0 + c >= a.N) return 0.f;
-            if constexpr (ES == 2) return __bfloat162float(__ldg(reinterpret_cast<const __nv_bfloat16*>(a.bias) + bcol0 + c));
-            else return __ldg(reinterpret_cast<const float*>(a.bias) + bcol0 + c);
-          };
-          float mx = -INFINITY;
-          int am = 0;
-          for (int c0 = 0; c0 < a.BN; c0 += 32) {
-            uint32_t v[32];
-            tmem_ld32(tbase + c0, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const float z = __uint_as_float(v[c]) + (has_bias ? bias_at(c0 + c) : 0.f);
-              if (c0 + c < ncol && z > mx) {  // strict: ties keep the lowest class
-                mx = z;
-                am = c0 + c;
-              }
-            }
-          }
-          long long yl = -1;
-          if (rv) yl = static_cast<long long>(a.labels[row]) - a.class_offset - static_cast<long long>(nb) * a.BN;
-          const float mxl = mx * kLog2e;
-          float s = 0.f, zy = 0.f;
-          // pass 2: P~ = exp(z - m_tile) -> tile store (bf16, or fp32 for ES=4); s_tile; z_y
-          constexpr int kChunk = kRowBytes / ES;  // P~ columns per 128-byte smem row
-          for (int c0 = 0; c0 < a.BN; c0 += kChunk) {
-            uint32_t v[64];
-            tmem_ld32(tbase + c0, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-            if constexpr (kChunk == 64) tmem_ld32(tbase + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
-            tmem_ld_wait();
-            if (c0 + kChunk >= a.BN) {
-              tc_fence_before();
-              mbar_arrive(&tempty[acc]);
-            }
-            uint32_t pk[32];
-#pragma unroll
-            for (int c = 0; c < kChunk; c += 2) {
-              const float z0 = __uint_as_float(v[c]) + (has_bias ? bias_at(c0 + c) : 0.f);
-              const float z1 = __uint_as_float(v[c + 1]) + (has_bias ? bias_at(c0 + c + 1) : 0.f);
-              const float p0 = (c0 + c < ncol) ? ex2_approx(fmaf(z0, kLog2e, -mxl)) : 0.f;
-              const float p1 = (c0 + c + 1 < ncol) ? ex2_approx(fmaf(z1, kLog2e, -mxl)) : 0.f;
-              s += p0 + p1;
-              if (c0 + c == yl) zy = z0;
-              if (c0 + c + 1 == yl) zy = z1;
-              if constexpr (ES == 2) {
-                pk[c >> 1] = pack_bf16x2(p0, p1);
-              } else {
-                pk[c] = __float_as_uint(p0);
-                pk[c + 1] = __float_as_uint(p1);
-              }
-            }
-            if (lane == 0) bulk_wait_read_n(nbuf);
-            __syncwarp();
-            uint8_t* b = ebuf + buf * kEpiBufBytes + lane * 128;
-#pragma unroll
-            for (int ch = 0; ch < 8; ++ch)
-              *reinterpret_cast<uint4*>(b + ((ch ^ (lane & 7)) << 4)) =
-                  make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              tma_store_2d(&tmOut, ebuf + buf * kEpiBufBytes, nb * a.BN + c0, row0);
-              bulk_commit();
-            }
-            if (++buf == nbuf) buf = 0;
-          }
-          if (rv) {
-            a.m_tile[static_cast<size_t>(row) * a.n_blocks + nb] = mx;
-            a.s_tile[static_cast<size_t>(row) * a.n_blocks + nb] = s;
-            if (a.a_tile != nullptr)
-              a.a_tile[static_cast<size_t>(row) * a.n_blocks + nb] =
-                  static_cast<int32_t>(a.class_offset + static_cast<long long>(nb) * a.BN + am);
-            if (yl >= 0 && yl < ncol) a.zy[row] = zy;
-          }
-        }
-      } else {
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
       }
       if constexpr (EPI == EPI_STORE_F32) {
         if (a.fix_mode != FIX_NONE) {

@@ -354,9 +354,12 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
       float m, s;
       row_stats(a, i, m, s, red);
       if (tslot >= 0) g_dbg_ts[tslot + 1] = gtime_ns();
-      const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : a.m_tile + static_cast<size_t>(i) * a.T;
-      const int top = argmax_tile(mx, a.T, m, redi);  // this rank's top-1 tile for the row
-      const int top_class = a.a_tile[static_cast<size_t>(i) * a.T + top];
+      int top_class = 0;
+      if (a.a_tile != nullptr) {  // predictions requested: this rank's top-1 tile for the row
+        const float* mx = a.mx_tile ? a.mx_tile + static_cast<size_t>(i) * a.T : a.m_tile + static_cast<size_t>(i) * a.T;
+        const int top = argmax_tile(mx, a.T, m, redi);
+        top_class = a.a_tile[static_cast<size_t>(i) * a.T + top];
+      }
       if (threadIdx.x < a.world) {  // thread p pushes the record to peer p
         if (threadIdx.x == 0 && (y < 0 || y >= a.C)) atomicOr(a.err, ERR_LABEL);
         const bool own = (y >= a.o_r) && (y < a.o_r + a.C_r);

@@ -215,7 +215,7 @@ struct Plan {
 };
 
 static constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100 (static + dynamic)
-static constexpr int kStaticSmemSlack = 128;  // the GEMM's own __shared__ words
+static constexpr int kStaticSmemSlack = 1664;  // the GEMM's own __shared__ words (logits epilogue: 1.5 KB)
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 static int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
@@ -538,7 +538,6 @@ struct whale_splitfc_ctx {
   bool fused_bwd = true;             // dW + dX in one persistent launch (bf16)
   bool gfuse = true;                 // G-fused backward (NEXT-4b): G formed from P~ in the bwd operand path
   bool row_bulk = false;             // dW tiles stored as 1-D bulk row copies (bwd_sm100.cuh)
-  bool w_l2 = false;                 // plain path: W_r kept L2-resident from the logits to the dX pass
   bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
@@ -598,10 +597,11 @@ static whale_status_t launch_gemm(whale_splitfc_ctx* c, int slot, const GemmCfg&
     const whale_status_t st = ensure_smem_attr(kern, slot);
     if (st != WHALE_OK) return st;
   }
-  if (g.cluster <= 1) return launch(c, kern, dim3(g.grid), dim3(kGemmThreads), g.smem, s, A, B, O, args);
+  constexpr int kThreads = EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGemmThreads;
+  if (g.cluster <= 1) return launch(c, kern, dim3(g.grid), dim3(kThreads), g.smem, s, A, B, O, args);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g.grid);
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = g.smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -759,13 +759,6 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   }
   c->fused_bwd = p.es == 2 && env_int("WHALE_FUSED_BWD", 1) != 0 && g_store_mode == 1;
   c->gfuse = c->fused_bwd && env_int("WHALE_GFUSE", 0) != 0;
-  {
-    // WHALE_W_L2=1: on the plain path the logits load W_r with evict_last and the backward's dX
-    // units (its second and last reader, scheduled first) with evict_first, so a shard that
-    // fits in the 126 MB L2 is read from HBM once per step.  Measured at c2 N = 4 (W_r = 102 MB):
-    // step 144 -> 164 us (the pinned lines crowd out P~ / dW traffic) -- off by default.
-    c->w_l2 = !p.f1 && c->fused_bwd && env_int("WHALE_W_L2", 0) == 1;
-  }
   if (p.dw_bf16 && !c->fused_bwd) {
     delete c;
     return fail(WHALE_ERR_UNSUPPORTED, "bf16 dW needs the fused backward (WHALE_FUSED_BWD / WHALE_STORE_MODE overrides)");
@@ -960,7 +953,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.m_tile = wsp<float>(c, L.m_tile);
     a.s_tile = wsp<float>(c, L.s_tile);
     a.zy = wsp<float>(c, L.zy);
-    a.a_tile = wsp<int32_t>(c, L.a_tile);
+    a.a_tile = pred != nullptr ? wsp<int32_t>(c, L.a_tile) : nullptr;  // top-1 only when asked for
     a.mx_tile = wsp<float>(c, L.mx_tile);
     a.upart = wsp<float>(c, L.upart);
     a.uref = wsp<float>(c, L.uref);
@@ -995,8 +988,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.dev_epoch = dev_epoch;
     a.labels = yg;
     a.bias = bias;
-    a.a_tile = wsp<int32_t>(c, L.a_tile);
-    a.b_keep_l2 = c->w_l2 ? 1 : 0;
+    a.a_tile = pred != nullptr ? wsp<int32_t>(c, L.a_tile) : nullptr;  // top-1 only when asked for
     a.class_offset = p.o_r;
     a.m_tile = wsp<float>(c, L.m_tile);
     a.s_tile = wsp<float>(c, L.s_tile);
@@ -1039,7 +1031,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.row_loss_local = row_loss;
     a.counter = counters + CNT_STATS;
     a.err = err;
-    a.a_tile = wsp<int32_t>(c, L.a_tile);
+    a.a_tile = pred != nullptr ? wsp<int32_t>(c, L.a_tile) : nullptr;  // top-1 only when asked for
     a.mx_tile = p.f1 ? wsp<float>(c, L.mx_tile) : nullptr;
     a.pred_local = pred;
     a.prob_local = prob;
@@ -1246,7 +1238,6 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       gf.inv_bt = static_cast<float>(1.0 / static_cast<double>(p.Bt));
     }
     b.row_bulk = c->row_bulk ? 1 : 0;
-    b.w_last_use = c->w_l2 ? 1 : 0;
     b.dw_bf16 = p.dw_bf16 ? 1 : 0;
     b.dw_ptr = dw;
     b.dw_ld = static_cast<int>(p.D);
