@@ -89,9 +89,9 @@ struct GemmArgs {
   int rs_signal;            // 1: this launch ends the step at N > 1 -> raise the RS flags
   int store_mode;           // EPI_STORE_F32: 0 per-warp TMA box, 1 CTA-wide TMA box, 2 st.global
   int n_fastest;            // tile order: 0 = M fastest (share B), 1 = N fastest (share A)
-  int cluster;              // 1, or 2: CTA pairs take M-adjacent tiles and TMA-multicast B
-                            // (each CTA loads half of the B tile into both CTAs' smem);
-                            // num_tiles then counts pair tiles (m_blocks must be even)
+  int cluster;              // 1, or 2: CTA pairs run M = 256 tcgen05.mma.cta_group::2 tiles over
+                            // M-adjacent blocks (each CTA holds its 128 rows of A and half of
+                            // B; only CTA 0 issues); num_tiles then counts pair tiles
   int debug;                // timing experiments only: bit0 skip stores, bit1 skip TMEM loads
   float* st_out;            // store_mode 2: output base ([splits x] M x N fp32)
   int* err;
@@ -137,6 +137,14 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, int tile, int& mb
   }
   kb0 = sp * a.kb_per_split;
   kb1 = min(kb0 + a.kb_per_split, a.num_kb);
+}
+
+// Hand an accumulator back to the MMA issuer: every epilogue thread arrives on tempty -- in a
+// CTA pair on the LEADER's barrier (its MMA overwrites both CTAs' halves).
+__device__ __forceinline__ void release_acc(uint64_t* tempty_acc, bool pair) {
+  tc_fence_before();
+  if (pair) mbar_arrive_remote_release(mapa_smem(smem_u32(tempty_acc), 0));
+  else mbar_arrive(tempty_acc);
 }
 
 // Unit -> tile for a CTA of rank `crank` in its cluster: with pairs (cluster = 2) a unit is
@@ -261,7 +269,7 @@ __device__ __forceinline__ void end_of_step_ticket(const GemmArgs& a, uint32_t e
 template <int ES>
 __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUtensorMap& tmOut, uint32_t tmem_base,
                                                    uint8_t* epi_smem, uint64_t* tfull, uint64_t* tempty, int unit0,
-                                                   int ustride, uint32_t crank, int warp, int lane) {
+                                                   int ustride, uint32_t crank, int warp, int lane, bool pair) {
   // 1.5 KB of static smem (the GEMM's stage budget leaves ~1.7 KB): s_x[g][r] holds group g's
   // row max after pass 1; after pass 2 group 1 puts its partial sum into s_x[0][r] (a slot only
   // thread (1, r) reads, and already has) and its first-max column into s_arg1[r]
@@ -411,8 +419,7 @@ __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUte
         if (++buf == nbw) buf = 0;
       }
     }
-    tc_fence_before();
-    mbar_arrive(&tempty[acc]);  // this thread's TMEM reads of the tile are done (256 arrivals)
+    release_acc(&tempty[acc], pair);  // this thread's TMEM reads of the tile are done (256 arrivals)
     if (has_zy) a.zy[row] = zy;
     const float my_sum = (sk[0] + sk[1]) + (sk[2] + sk[3]);
     if (g == 1) {
@@ -438,7 +445,9 @@ __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUte
 // logit) is the slow side of the TMEM double buffer when K is short (c4: D = 512), so two
 // groups of 4 warps split each tile's column chunks (interleaved) and combine their row
 // max / sum / top-1 through shared memory.
-template <int EPI, bool A_MN, bool B_MN, int ES>
+// PAIR: the cta_group::2 instantiation (launched as 2-CTA clusters; a kernel that contains
+// cta_group::2 instructions cannot be launched without a cluster).
+template <int EPI, bool A_MN, bool B_MN, int ES, bool PAIR = false>
 __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGemmThreads, 1)
     splitfc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmOut, const GemmArgs a) {
@@ -458,19 +467,19 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // CTA pairs (cluster = 2): unit u = pair tile, this CTA takes M block 2*mp + crank
-  const int cs = a.cluster;
+  constexpr int cs = PAIR ? 2 : 1;
   const uint32_t crank = cs > 1 ? cluster_ctarank() : 0u;
   const int unit0 = cs > 1 ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
   const int ustride = cs > 1 ? static_cast<int>(ncluster_x()) : static_cast<int>(gridDim.x);
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], cs);  // pairs: both CTAs' MMAs must release a stage (multicast B)
+      mbar_init(&full[i], 1);   // pairs: the leader's expect_tx; both CTAs' TMA bytes land here
+      mbar_init(&empty[i], 1);  // pairs: the leader's multicast commit
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EPI == EPI_FWD_STATS ? 256 : 128);
+      mbar_init(&tempty[i], (EPI == EPI_FWD_STATS ? 256 : 128) * cs);  // pairs: both CTAs' epilogues
     }
     fence_mbar_init();
   }
@@ -479,10 +488,13 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmOut);
   }
-  if (warp == 2) tmem_alloc(tmem_holder, kTmemCols);
+  if (cs > 1) cluster_sync();  // peer barriers initialised before any pair TMA / commit lands
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_pair(tmem_holder, kTmemCols);
+    else tmem_alloc(tmem_holder, kTmemCols);
+  }
   tc_fence_before();
   __syncthreads();
-  if (cs > 1) cluster_sync();  // peer barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   pdl_wait();      // everything below reads/writes memory the previous kernel may touch
@@ -504,8 +516,11 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
       const int box_bytes = bk * kRowBytes;
       const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
-      const uint32_t tx = static_cast<uint32_t>((WHALE_SKIP(a.debug & 8) ? 0 : a_bytes) +
-                                                (B_MN ? (a.BN / kAtom) * box_bytes : a.BN * kRowBytes));
+      // pairs: this CTA's half of B; the leader expects both CTAs' bytes
+      const int bn_cta = a.BN / cs;
+      const uint32_t tx = static_cast<uint32_t>(cs) *
+                          static_cast<uint32_t>((WHALE_SKIP(a.debug & 8) ? 0 : a_bytes) +
+                                                (B_MN ? (bn_cta / kAtom) * box_bytes : bn_cta * kRowBytes));
       for (int tile = unit0; tile < a.num_tiles; tile += ustride) {
         int mb, nb, sp, kb0, kb1;
         decode_unit(a, tile, crank, mb, nb, sp, kb0, kb1);
@@ -513,6 +528,31 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
           mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* sA = smem + stage * a.stage_bytes;
           uint8_t* sB = sA + a_bytes;
+          if constexpr (PAIR) {
+            // pair: both CTAs load their own A rows and their half of B into their own smem;
+            // the bytes complete on the leader's full barrier, which the leader alone arms
+            const uint32_t fl = mapa_smem(smem_u32(&full[stage]), 0);
+            if (crank == 0) mbar_arrive_expect_tx(&full[stage], tx);
+            if (!A_MN) {
+              tma_load_2d_pair(sA, &tmA, fl, kb * kBK, mb * kBM);
+            } else {
+#pragma unroll
+              for (int j = 0; j < kBM / kAtom; ++j)
+                tma_load_2d_pair(sA + j * box_bytes, &tmA, fl, mb * kBM + j * kAtom, kb * bk);
+            }
+            if (!B_MN) {  // tmB box = {kBK, BN/2}
+              tma_load_2d_pair(sB, &tmB, fl, kb * kBK, nb * a.BN + static_cast<int>(crank) * bn_cta);
+            } else {
+              for (int j = 0; j < bn_cta / kAtom; ++j)
+                tma_load_2d_pair(sB + j * box_bytes, &tmB, fl, nb * a.BN + static_cast<int>(crank) * bn_cta + j * kAtom,
+                                 kb * bk);
+            }
+            if (++stage == a.stages) {
+              stage = 0;
+              phase ^= 1u;
+            }
+            continue;
+          }
           mbar_arrive_expect_tx(&full[stage], tx);
           if (WHALE_SKIP(a.debug & 8)) {
             // timing experiment: A operand not loaded
@@ -523,17 +563,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
             for (int j = 0; j < kBM / kAtom; ++j)
               tma_load_2d(sA + j * box_bytes, &tmA, &full[stage], mb * kBM + j * kAtom, kb * bk);
           }
-          if (cs > 1) {
-            // B is shared by the pair: this CTA loads its half and multicasts it to both
-            if (!B_MN) {  // tmB box = {kBK, BN/2}
-              const int half = a.BN / 2;
-              tma_load_2d_mc(sB + crank * half * kRowBytes, &tmB, &full[stage], kb * kBK,
-                             nb * a.BN + static_cast<int>(crank) * half, 0x3);
-            } else {
-              for (int j = static_cast<int>(crank); j < a.BN / kAtom; j += 2)
-                tma_load_2d_mc(sB + j * box_bytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * bk, 0x3);
-            }
-          } else if (!B_MN) {
+          if (!B_MN) {
             tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
           } else {
             for (int j = 0; j < a.BN / kAtom; ++j)
@@ -547,9 +577,9 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      const uint32_t idesc = umma_idesc(kBM, a.BN, A_MN, B_MN, ES == 2 ? 1u : 2u);
+    // ===================== MMA issuer (pairs: the leader only, M = 256) =====================
+    if (lane == 0 && crank == 0) {
+      const uint32_t idesc = umma_idesc(kBM * cs, a.BN, A_MN, B_MN, ES == 2 ? 1u : 2u);
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
       const uint32_t box_bytes = bk * kRowBytes;
       const uint32_t a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
@@ -576,21 +606,27 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
                                      : umma_sdesc(aS + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? umma_sdesc(bS + k * kKStepMN, box_bytes, 1024)
                                      : umma_sdesc(bS + k * 32, 16, 1024);
-            if constexpr (ES == 2)
+            if constexpr (PAIR) {
+              if constexpr (ES == 2)
+                umma_bf16_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+              else
+                umma_tf32_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            } else if constexpr (ES == 2) {
               umma_bf16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-            else
+            } else {
               umma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
           }
-          // frees this smem stage once the MMAs have read it (pairs: in both CTAs, since the
-          // peer multicasts its half of B into this stage too)
-          if (cs > 1) umma_commit_mc(&empty[stage], 0x3);
+          // frees this smem stage (pairs: in both CTAs) once the MMAs have read it
+          if constexpr (PAIR) umma_commit_pair_mc(&empty[stage], 0x3);
           else umma_commit(&empty[stage]);
           if (++stage == a.stages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if constexpr (PAIR) umma_commit_pair_mc(&tfull[acc], 0x3);  // both halves ready
+        else umma_commit(&tfull[acc]);                     // accumulator ready for the epilogue
       }
     }
   } else if (EPI == EPI_FWD_STATS && warp >= 4) {
@@ -600,7 +636,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
     if (a.wait_flags != nullptr && threadIdx.x == 128)
       for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
     named_bar_sync(2, 256);
-    fwd_stats_epilogue<ES>(a, tmOut, tmem_base, epi_smem, tfull, tempty, unit0, ustride, crank, warp, lane);
+    fwd_stats_epilogue<ES>(a, tmOut, tmem_base, epi_smem, tfull, tempty, unit0, ustride, crank, warp, lane, cs > 1);
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
@@ -635,8 +671,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
             }
             if (do_scale) scale32(v, gsc);
             if (c0 + 32 >= a.BN) {
-              tc_fence_before();
-              mbar_arrive(&tempty[acc]);
+              release_acc(&tempty[acc], cs > 1);
             }
             if (WHALE_SKIP(a.debug & 1)) continue;
             if (threadIdx.x == 128) bulk_wait_read_n(nbuf);
@@ -663,8 +698,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
             tmem_ld32(tbase + c0, v);
             tmem_ld_wait();
             if (c0 + 32 >= a.BN) {
-              tc_fence_before();
-              mbar_arrive(&tempty[acc]);
+              release_acc(&tempty[acc], cs > 1);
             }
             if (do_scale) scale32(v, gsc);
             const int col = nb * a.BN + c0;
@@ -683,8 +717,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
             tmem_ld32(tbase + c0, v);
             tmem_ld_wait();
             if (c0 + 32 >= a.BN) {  // accumulator fully read: hand TMEM back to the MMA warp
-              tc_fence_before();
-              mbar_arrive(&tempty[acc]);
+              release_acc(&tempty[acc], cs > 1);
             }
             if (do_scale) scale32(v, gsc);
             if (lane == 0) bulk_wait_read_n(nbuf);  // the store that last used this buffer has read it
@@ -703,8 +736,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
             if (++buf == nbuf) buf = 0;
           }
         } else {
-          tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          release_acc(&tempty[acc], cs > 1);
         }
       }
       if constexpr (EPI == EPI_STORE_F32) {
@@ -739,7 +771,8 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
   if (cs > 1) cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kTmemCols);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem_base, kTmemCols);
+    else tmem_dealloc(tmem_base, kTmemCols);
   }
   if (a.bump_epoch) end_of_step_ticket(a, e, s_fix_go);
 }

@@ -163,21 +163,34 @@ struct GemmCfg {
 };
 
 static int env_int(const char* name, int dflt);
+static constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100 (static + dynamic)
+static constexpr int kStaticSmemSlack = 1664;  // the GEMM's own __shared__ words (logits epilogue: 1.5 KB)
 
-// Pair M-adjacent tiles in 2-CTA clusters when the tile grid allows it (even m_blocks, B
-// tile splittable in halves / atom pairs); grid = 2 x pair tiles, capped at the SM count.
-static void maybe_pair(GemmCfg& g, int sms, bool b_mn, int atom) {
-  // off by default: measured neutral for the logits (c5: tensor-bound at the sustained
-  // peak) and +3% for the standalone dW GEMM; kept as an option (WHALE_CLUSTER=1)
-  const bool ok = env_int("WHALE_CLUSTER", 0) != 0 && g.m_blocks >= 2 &&
-                  (b_mn ? (g.BN / atom) % 2 == 0 : (g.BN / 2) % 16 == 0) && g.splits == 1;
+// CTA pairs (cta_group::2): M-adjacent tiles run as one M = 256 MMA; each CTA keeps its 128
+// rows of A and HALF of the B tile, so a stage costs a_bytes + B/2 and more stages fit.  The
+// grid is 2 x pair tiles (capped at the SM count); an odd M block count gets one all-padding
+// tile (TMA zero-fills its loads, clips its stores).  WHALE_CLUSTER=2 forces pairs, 1 forbids
+// them; by default (-1) the logits pair up when K is long (>= 32 k-blocks: the tensor-bound
+// c5, where pairs take the logits from 0.84 to 0.91 of the burst bf16 peak) -- with a short K the
+// two-pass softmax epilogue, not the operand feed, sets the pace and pairs lose (c4: -13 %).
+static void maybe_pair(GemmCfg& g, int sms, bool b_mn, int atom, int es = 2, bool auto_ok = false) {
+  const int want = env_int("WHALE_CLUSTER", -1);
+  const bool on = want == 2 || (want < 0 && auto_ok && g.num_kb >= 32);
+  const bool ok = on && g.m_blocks >= 2 && (b_mn ? (g.BN / atom) % 2 == 0 : (g.BN / 2) % 16 == 0) && g.splits == 1;
   if (!ok) return;
   g.cluster = 2;
-  // an odd M block count gets one all-padding tile (TMA zero-fills its loads, clips its stores)
   g.m_blocks += g.m_blocks & 1;
   g.num_tiles = g.m_blocks * g.n_blocks * g.splits;
   const int units = g.num_tiles / 2;
   g.grid = 2 * std::min(units, sms / 2);
+  // per-CTA stage: own A + half of B
+  const int box = g.bk * kRowBytes;
+  const int a_bytes = (b_mn ? (kBM / atom) * box : kStageABytes);
+  g.stage_bytes = a_bytes + (b_mn ? (g.BN / 2 / atom) * box : (g.BN / 2) * kRowBytes);
+  const int avail = kSmemLimit - kStaticSmemSlack - 1024 - 256 - 4 * g.epi_bufs * kEpiBufBytes;
+  g.stages = std::min(8, avail / g.stage_bytes);
+  g.smem = gemm_smem_bytes(g.stages, g.stage_bytes, g.epi_bufs);
+  (void)es;
 }
 
 struct Layout {
@@ -214,8 +227,6 @@ struct Plan {
   Layout L;
 };
 
-static constexpr int kSmemLimit = 232448;  // 227 KB opt-in per CTA on sm_100 (static + dynamic)
-static constexpr int kStaticSmemSlack = 1664;  // the GEMM's own __shared__ words (logits epilogue: 1.5 KB)
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 static int cdiv(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b); }
@@ -356,7 +367,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   const int kbk = kRowBytes / p.es;   // K elements per stage
   const int atom = kRowBytes / p.es;  // MN-major atom / fwd P~ chunk
   p.fwd = choose_plain(p.Bt, p.Cr, p.D, atom, kbk, sms);
-  maybe_pair(p.fwd, sms, false, atom);
+  maybe_pair(p.fwd, sms, false, atom, p.es, p.es == 2);
   {
     // dW: both operands MN-major; a short K (= B_tot <= 32) uses 32-row K stages (no
     // zero-padded half stage), which doubles the pipeline depth for the same smem.
@@ -570,9 +581,10 @@ static whale_status_t launch(whale_splitfc_ctx* c, void (*kern)(KArgs...), dim3 
 }
 
 // cudaFuncSetAttribute acts on the current device: remember per (device, kernel slot) that the
-// opt-in shared-memory limit has been raised (slots 0..7: GEMMs, 8 / 9: fused backward fp32 / bf16 dW).
+// opt-in shared-memory limit has been raised (slots 0..7: GEMMs, 8 / 9: fused backward fp32 / bf16 dW,
+// 10..17: the GEMMs' CTA-pair instantiations).
 static constexpr int kMaxDevices = 64;
-static bool g_attr_done[kMaxDevices][10] = {};
+static bool g_attr_done[kMaxDevices][20] = {};
 
 template <typename K>
 static whale_status_t ensure_smem_attr(K kern, int slot) {
@@ -592,9 +604,9 @@ template <int EPI, bool AMN, bool BMN, int ES>
 static whale_status_t launch_gemm(whale_splitfc_ctx* c, int slot, const GemmCfg& g, const CUtensorMap& A,
                                   const CUtensorMap& B, const CUtensorMap& O, const GemmArgs& args,
                                   cudaStream_t s) {
-  auto kern = splitfc_gemm_kernel<EPI, AMN, BMN, ES>;
+  auto kern = g.cluster > 1 ? splitfc_gemm_kernel<EPI, AMN, BMN, ES, true> : splitfc_gemm_kernel<EPI, AMN, BMN, ES, false>;
   {
-    const whale_status_t st = ensure_smem_attr(kern, slot);
+    const whale_status_t st = ensure_smem_attr(kern, slot + (g.cluster > 1 ? 10 : 0));
     if (st != WHALE_OK) return st;
   }
   constexpr int kThreads = EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGemmThreads;
@@ -690,6 +702,11 @@ static whale_status_t preload_kernels() {
       reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, true, true, 2>),
       reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, false, true, 2>),
       reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, false, false, 4>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_FWD_STATS, false, false, 2, true>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_FWD_STATS, false, false, 4, true>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, true, true, 2, true>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, false, true, 2, true>),
+      reinterpret_cast<const void*>(splitfc_gemm_kernel<EPI_STORE_F32, false, false, 4, true>),
       reinterpret_cast<const void*>(splitfc_fwd_dx_kernel),
       reinterpret_cast<const void*>(splitfc_bwd_kernel<2, false>),
       reinterpret_cast<const void*>(splitfc_bwd_kernel<2, true>),
@@ -780,7 +797,12 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     c->bwd_smem = fixed + c->bwd_stages * c->bwd_stage_bytes;
     if (c->bwd_stages < 2) c->fused_bwd = false;
   }
-  if (!c->fused_bwd && p.es == 2) maybe_pair(c->p.dw, sms, true, kRowBytes / p.es);  // standalone dW GEMM
+  if (!c->fused_bwd && p.es == 2) {
+    maybe_pair(c->p.dw, sms, true, kRowBytes / p.es);  // standalone dW GEMM
+    // standalone dX GEMM (only without split-K and with whole pairs of M blocks: the split-K
+    // tile counters were laid out for the unpaired grid)
+    if (p.dx.splits == 1 && p.dx.m_blocks % 2 == 0) maybe_pair(c->p.dx, sms, true, kRowBytes / p.es);
+  }
   if (p.f1) {
     // F1 clusters must all be co-resident (one wave): not every GPC holds a multiple of KC SMs
     cudaFuncAttributes fa{};

@@ -439,6 +439,37 @@ def test_forward_only_steps(whale, B, D, C):
     op.close()
 
 
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("B,D,C", [(200, 520, 3001), (300, 1024, 20_000), (129, 136, 777), (256, 2048, 10_000)])
+def test_cta_pair_mma(whale, B, D, C, fused, monkeypatch):
+    """CTA pairs (tcgen05.mma.cta_group::2, M = 256, each CTA holding half of B): forced on for
+    the logits (and, with the unfused backward, the standalone dW / dX GEMMs) at small shapes
+    incl. an odd M-block count (padding tile) -- against the oracle, with bias and predictions."""
+    monkeypatch.setenv("WHALE_CLUSTER", "2")
+    monkeypatch.setenv("WHALE_FUSED_BWD", fused)
+    seed = 900 + B
+    X = syn.gen_features((0, B), D, seed, "bf16")
+    W = syn.gen_weight((0, C), D, seed, "peaked", "bf16")
+    b = syn.gen_bias((0, C), seed, 2.0, "bf16")
+    y = syn.gen_labels((0, B), C, seed)
+    op = whale.SplitFCSoftmaxCE(C, D, B)
+    assert op.config()["fwd"]["cluster"] == 2
+    xd, wd = X.cuda(), W.cuda()
+    loss = float(op.forward(xd, y.cuda(), wd, row_loss=True, bias=b.cuda(), predictions=True))
+    dx, dw, db = op.backward(wd, bias_grad=True)
+    op.check()
+    f = oracle.forward_backward(X, W, y.numpy(), b)
+    assert abs(loss - f["loss"]) <= LOSS_RTOL * f["loss"]
+    np.testing.assert_allclose(op.row_loss.cpu().numpy(), f["row_loss"], rtol=LOSS_RTOL, atol=LOSS_RTOL)
+    assert _fro(dx.float().cpu(), f["dX"]) <= FRO_RTOL
+    assert _fro(dw.cpu(), f["dW"]) <= FRO_RTOL
+    assert _fro(db.cpu(), f["db"]) <= FRO_RTOL
+    Z = np.sort(f["Z"], axis=1)
+    clear = (Z[:, -1] - Z[:, -2]) > 1e-3
+    assert np.array_equal(op.pred.cpu().numpy()[clear], f["pred"][clear])
+    op.close()
+
+
 @pytest.mark.parametrize("B,D,C", [(32, 1024, 9001), (200, 520, 3001), (300, 1024, 20_000)])
 def test_gfused_backward_matches_materialised(whale, B, D, C, monkeypatch):
     """NEXT-4b: the G-fused backward (G formed from P~ in the operand path) computes the same
