@@ -226,3 +226,25 @@ def test_emulated_dead_peer_reports_comm(whale, B, D):
     finally:
         for op in ops:
             op.close()
+
+
+def test_emulated_random_fuzz(whale):
+    """Seeded random multi-rank cases: world 2-4, uneven batches (zero-row ranks allowed),
+    capacity-proportional class shards, both paths (F1 whenever B_tot <= 32 and D % 256 == 0),
+    bias / predictions; 2 steps of new inputs each, every step against the oracle."""
+    rng = np.random.default_rng(2011_0920)
+    for case in range(8):
+        world = int(rng.integers(2, 5))
+        f1 = case % 2 == 0
+        if f1:
+            batch = [int(v) for v in rng.multinomial(int(rng.integers(world, 33)), [1.0 / world] * world)]
+            D = int(rng.choice([256, 512, 768, 1024]))
+        else:
+            batch = [int(v) for v in rng.integers(0, 48, world)]
+            D = int(rng.integers(1, 64)) * 8
+        if sum(batch) == 0:
+            batch[0] = 1
+        C = int(rng.integers(world * 8, 12_000))
+        cap = [int(v) for v in rng.integers(1, 4, world)] if rng.integers(0, 2) else None
+        run_emulated(whale, world, D=D, C=C, batch=batch, capacity=cap, regime=str(rng.choice(["init", "peaked"])),
+                     bias=bool(rng.integers(0, 2)), steps=2, seed=3000 + case)
