@@ -251,6 +251,9 @@ def main():
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for a, b in evs:
             flush()  # > L2: evicts the previous step's working set (outside the events)
+            # N > 1: the step's exchanges couple the ranks, so a rank whose flush ends first
+            # would count its peers' flush as step time: align the ranks on the device first
+            op.device_barrier()
             a.record(s)
             run()
             b.record(s)

@@ -153,6 +153,12 @@ class SplitFCSoftmaxCE:
             return dx_local, dw_shard, db_shard
         return dx_local, dw_shard
 
+    def device_barrier(self):
+        """World > 1: a device-side barrier of all ranks on the current stream (torch symmetric
+        memory's signal pads) -- aligns the ranks before a timed step (bench.py)."""
+        if self.world > 1 and isinstance(self._symm, tuple):
+            self._symm[1].barrier(channel=0)
+
     def check(self):
         _lib.whale_splitfc_check(self.ctx, torch.cuda.current_stream(self.device).cuda_stream)
 
