@@ -432,7 +432,7 @@ def main():
                    "dirty flush lines are written back inside a step)" if flush_l2
                    else f"inputs larger than L2 (W shard {w_bytes / 2 ** 20:.0f} MiB > 2x126 MiB)"),
             "tiles": {k: cfgj[k] for k in ("fwd", "dw", "dx")},
-            "launch": "eager" if args.no_graph else "CUDA graph per step (PDL edges)",
+            "launch": "eager" if args.no_graph else "CUDA graph per step",
         },
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": X.numel() * X.element_size() + y.numel() * 4,

@@ -27,8 +27,9 @@
 //                  written as the final dX (N = 1) or pushed over NVLink into the owner
 //                  rank's receive slab (N > 1, fused GEMM -> reduce-scatter).
 //
-// All kernels use programmatic dependent launch: the prologue (barrier init, TMEM alloc,
-// descriptor prefetch) overlaps the previous kernel's tail.
+// Every kernel is PDL-ready (griddepcontrol.wait after its prologue -- barrier init, TMEM
+// alloc, descriptor prefetch); the host launches with programmatic dependent launch only on
+// request (WHALE_PDL=1: measured slower in round 2).
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>

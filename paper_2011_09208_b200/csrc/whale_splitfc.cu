@@ -545,7 +545,7 @@ struct whale_splitfc_ctx {
   uint32_t epoch = 0;                // forward count (flag epochs, parity)
   uint32_t bwd_epoch = 0;            // backward count (fixup counters)
   bool have_fwd = false;
-  bool pdl = true;
+  bool pdl = false;
   bool fused_bwd = true;             // dW + dX in one persistent launch (bf16)
   bool gfuse = true;                 // G-fused backward (NEXT-4b): G formed from P~ in the bwd operand path
   bool row_bulk = false;             // dW tiles stored as 1-D bulk row copies (bwd_sm100.cuh)
@@ -768,7 +768,10 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   // turn (no PDL) and the exchange kernels keep bounded grids; combine with
   // WHALE_SM_LIMIT_R<r> so every rank's persistent grid fits beside the others.
   c->shared_device = env_int("WHALE_SHARED_DEVICE", 0) != 0;
-  c->pdl = !(pdl_env && pdl_env[0] == '0') && !c->shared_device;
+  // programmatic dependent launch: off by default -- measured slower in every configuration
+  // (c2 N=1 249.0 -> 248.1 us, N=2 194 -> 189, c4 1265 -> 1176, c5 10.65 -> 10.38 ms without
+  // it); WHALE_PDL=1 turns it on (the kernels' griddepcontrol.wait keeps either mode correct)
+  c->pdl = (pdl_env && pdl_env[0] == '1') && !c->shared_device;
   {
     // peer-wait timeout (flags, LL records, split-K counters): WHALE_TIMEOUT_MS, default 300 s
     const unsigned long long ns = static_cast<unsigned long long>(std::max(1, env_int("WHALE_TIMEOUT_MS", 300000))) * 1000000ull;
