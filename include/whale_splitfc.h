@@ -133,6 +133,13 @@ typedef struct whale_splitfc_desc {
    * order); B_r may be 0 when world > 1 (that rank then only serves its class shard);
    * sum B_r >= 1.  whale_splitfc_plan(B_tot, world, capacity) gives the proportional split. */
   const int64_t* batch_counts;
+  /* NVLS (NVLink SHARP) multicast address of the symmetric buffer (world > 1), or NULL: one
+   * multimem store then reaches the same offset in every rank's buffer through the NVSwitch.
+   * Used for the bridge all-gather (A2) of X_r, y_r and its flags (the B200
+   * form of the all-gather the paper's bridge inserts); NULL keeps the
+   * unicast peer stores.  The reduce-scatter stays unicast (its fixed summation order keeps
+   * dX bitwise reproducible; a switch reduction would not). */
+  void* multicast_ptr;
 } whale_splitfc_desc;
 
 typedef struct whale_splitfc_ctx whale_splitfc_ctx;

@@ -49,6 +49,7 @@ class Desc(ctypes.Structure):
         ("local_workspace", ctypes.c_void_p),
         ("local_workspace_bytes", ctypes.c_size_t),
         ("batch_counts", ctypes.POINTER(ctypes.c_int64)),
+        ("multicast_ptr", ctypes.c_void_p),
     ]
 
 
@@ -145,7 +146,7 @@ def whale_splitfc_plan_mem(num_classes: int, world_size: int, capacity=None, mem
 
 
 def make_desc(rank, world, B, D, C, counts, offsets, x_dtype=WHALE_BF16, peer_ptrs=None, symm_bytes=0,
-              workspace_ptr=0, workspace_bytes=0, batch_counts=None, dw_dtype=WHALE_F32):
+              workspace_ptr=0, workspace_bytes=0, batch_counts=None, dw_dtype=WHALE_F32, multicast_ptr=0):
     """Build a Desc; the returned tuple keeps the ctypes arrays alive.  batch_counts: optional
     per-rank DP batch [world] (NEXT-3); B must then be batch_counts[rank]."""
     c_counts = (ctypes.c_int64 * world)(*counts)
@@ -156,7 +157,7 @@ def make_desc(rank, world, B, D, C, counts, offsets, x_dtype=WHALE_BF16, peer_pt
     c_batch = (ctypes.c_int64 * world)(*batch_counts) if batch_counts is not None else None
     d = Desc(rank, world, B, D, C, c_counts, c_offs, x_dtype, dw_dtype,
              ctypes.cast(c_peers, ctypes.POINTER(ctypes.c_void_p)) if c_peers is not None else None,
-             symm_bytes, workspace_ptr or None, workspace_bytes, c_batch)
+             symm_bytes, workspace_ptr or None, workspace_bytes, c_batch, multicast_ptr or None)
     return d, (c_counts, c_offs, c_peers, c_batch)
 
 

@@ -361,6 +361,23 @@ __device__ __forceinline__ void red_add_relaxed_sys(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// NVLS multimem (NVSwitch multicast): one store / reduction reaches the same offset in every
+// rank's buffer of a multicast object; `mc` is an address inside the multicast mapping.
+__device__ __forceinline__ void multimem_st_v4(void* mc, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void multimem_st_u32(void* mc, uint32_t v) {
+  asm volatile("multimem.st.relaxed.sys.global.b32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
+__device__ __forceinline__ void multimem_red_add_release_u32(void* mc, uint32_t v) {
+  asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
+__device__ __forceinline__ void multimem_red_add_relaxed_u32(void* mc, uint32_t v) {
+  asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+}
+
 // LL protocol word: {data (low 32), flag (high 32)} written by one aligned 64-bit store, which
 // is single-copy atomic -- the reader validates the data by its flag half (NCCL's LL idea).
 __device__ __forceinline__ void st_relaxed_sys_v2(uint2* p, uint32_t data, uint32_t flag) {

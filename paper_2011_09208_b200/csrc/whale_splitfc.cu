@@ -531,6 +531,7 @@ struct whale_splitfc_ctx {
   Plan p;
   uint8_t* ws = nullptr;
   uint8_t* symm[kMaxRanks] = {};
+  uint8_t* mc = nullptr;  // NVLS multicast address of the symmetric buffer (or NULL)
   // static maps (X maps: per parity at N > 1; cached on the caller's X at N = 1)
   CUtensorMap tmX_fwd, tmX_dw, tmP_store, tmG_dx, tmG_dw, tmDxPart;
   CUtensorMap tmGT, tmXT, tmWT;  // fp32 path: K-major transposed operands
@@ -761,6 +762,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
       return fail(WHALE_ERR_STATE, "symmetric buffers missing or < %zu bytes", p.L.symm_total);
     }
     for (int r = 0; r < p.world; ++r) c->symm[r] = static_cast<uint8_t*>(desc->peer_symm_ptrs[r]);
+    c->mc = static_cast<uint8_t*>(desc->multicast_ptr);
   }
   const char* pdl_env = getenv("WHALE_PDL");
   // WHALE_SHARED_DEVICE=1: several ranks share this device (the single-GPU multi-rank test
@@ -958,7 +960,10 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
              (launch(c, bridge_gather_kernel, dim3(grid), dim3(256), 0, s, static_cast<const uint4*>(x_local),
                      y_local, x_vecs, static_cast<int>(p.B), static_cast<int>(p.Boff[p.rank]),
                      static_cast<int64_t>(p.D * ES / 16), p.rank, p.world, dx, dy, fl,
-                     env_int("WHALE_GATHER_DBG", 0))));
+                     env_int("WHALE_GATHER_DBG", 0),
+                     c->mc ? reinterpret_cast<uint4*>(c->mc + L.xg) : nullptr,
+                     c->mc ? reinterpret_cast<int32_t*>(c->mc + L.yg) : nullptr,
+                     c->mc ? reinterpret_cast<uint32_t*>(c->mc + L.flags) + FLAG_GATHER * kMaxRanks + p.rank : nullptr)));
   }
   // ---- A3 logits GEMM with fused row statistics
   if (ES == 2 && p.f1) {
@@ -1450,6 +1455,7 @@ extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, cha
                   ",\"off_s_tile\":" + std::to_string(p.L.s_tile) + ",\"off_lse\":" + std::to_string(p.L.lse) +
                   ",\"off_dxpart\":" + std::to_string(p.L.dxpart) + ",\"f1\":" + std::to_string(p.f1 ? 1 : 0) +
                   ",\"f1_clusters\":" + std::to_string(p.f1_ncl) + ",\"f1_stages\":" + std::to_string(p.f1_stages) +
+                  ",\"nvls\":" + std::to_string(ctx->mc != nullptr ? 1 : 0) +
                   ",\"local_bytes\":" + std::to_string(p.L.local_total) +
                   ",\"symm_bytes\":" + std::to_string(p.L.symm_total) + "}";
   if (s.size() + 1 > buf_len) return fail(WHALE_ERR_INVALID_ARG, "buffer too small (%zu)", s.size() + 1);

@@ -74,6 +74,7 @@ class SplitFCSoftmaxCE:
         symm_bytes, local_bytes = _lib.whale_splitfc_workspace_size(q)
         self.workspace = torch.empty(local_bytes, dtype=torch.uint8, device=self.device)
         peer_ptrs = None
+        mc_ptr = 0
         self._symm = None
         if emulated is not None and self.world > 1:
             bufs = emulated[2]
@@ -91,9 +92,18 @@ class SplitFCSoftmaxCE:
             dist.barrier(group=group)
             peer_ptrs = [int(p) for p in hdl.buffer_ptrs]
             self._symm = (buf, hdl)
+            # NVLS multicast address of the symmetric buffer when the NVSwitch supports it
+            # (WHALE_NVLS=0 keeps the unicast all-gather)
+            try:
+                if os.environ.get("WHALE_NVLS", "1") != "0" and symm_mem._SymmetricMemory.has_multicast_support(
+                        torch._C._autograd.DeviceType.CUDA, self.device.index):
+                    mc_ptr = int(hdl.multicast_ptr or 0)
+            except Exception:
+                mc_ptr = 0
         self._desc, self._keep = _lib.make_desc(
             self.rank, self.world, self.B, self.D, self.C, self.counts, self.offsets, xdt, peer_ptrs, symm_bytes,
-            self.workspace.data_ptr(), local_bytes, self.batch_counts, dwdt)
+            self.workspace.data_ptr(), local_bytes, self.batch_counts, dwdt, mc_ptr)
+        self.nvls = bool(mc_ptr)
         self.ctx = _lib.whale_splitfc_create(self._desc)
         self.loss = torch.zeros((), dtype=torch.float32, device=self.device)
         self.row_loss = torch.zeros(self.B, dtype=torch.float32, device=self.device)

@@ -60,7 +60,7 @@ def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf1
         bit_equal = all(torch.equal(l, losses[0]) for l in losses)
         res = {
             "B": B, "batch": bc, "D": D, "C": C, "world": world, "capacity": capacity, "regime": regime, "dtype": dtype,
-            "C_r": c, "step": step, "loss": float(loss), "loss_ref": float(f["loss"]),
+            "C_r": c, "step": step, "nvls": op.config().get("nvls", 0), "loss": float(loss), "loss_ref": float(f["loss"]),
             "loss_rel": abs(float(loss) - f["loss"]) / abs(f["loss"]),
             "rowloss_rel": fro(op.row_loss.cpu(), f["row_loss"][r0:r0 + B]),
             "dx_rel": fro(dx.float().cpu(), f["dX"][r0:r0 + B]) if B else 0.0,
