@@ -10,7 +10,8 @@ import json
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libwhale_splitfc.so")
+# WHALE_LIB_PATH: an alternative build of the same library (timing-experiment builds, scripts/ only)
+LIB_PATH = os.environ.get("WHALE_LIB_PATH") or os.path.join(_HERE, "lib", "libwhale_splitfc.so")
 
 STATUS = {
     0: "WHALE_OK", 1: "WHALE_ERR_INVALID_ARG", 2: "WHALE_ERR_UNSPLITTABLE", 3: "WHALE_ERR_UNSUPPORTED",

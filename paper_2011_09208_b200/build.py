@@ -29,22 +29,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, timing: bool = False) -> str:
+    """timing=True: the timing-experiment variant (-DWHALE_TIMING_EXPERIMENTS: debug modes that
+    skip work) as lib/libwhale_splitfc_timing.so, loaded only via WHALE_LIB_PATH by scripts/."""
+    lib = LIB.replace(".so", "_timing.so") if timing else LIB
+    if not force and not timing and not _stale():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    extra = ["-DWHALE_TIMING_EXPERIMENTS"] if timing else []
+    cmd = [NVCC, *FLAGS, *extra, "-o", lib + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libwhale_splitfc.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
-        f.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    if not timing:
+        with open(os.path.join(LIBDIR, "ptxas.log"), "w") as f:
+            f.write(r.stderr)
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timing="--timing" in sys.argv))

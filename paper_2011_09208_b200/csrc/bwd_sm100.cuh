@@ -249,7 +249,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int dw_bk = W.bk;
       const int dw_box = dw_bk * kRowBytes;
       const int dw_a_bytes = (kBM / kAtom) * dw_box;
-      const uint32_t tx_dx = static_cast<uint32_t>(kStageABytes + (X.BN / kAtom) * kBK * kRowBytes);
+      const int dx_a_bytes = X.a_rows * kRowBytes;  // G rows per stage (B_tot rounded up to 8 when < 128)
+      const uint32_t tx_dx = static_cast<uint32_t>(dx_a_bytes + (X.BN / kAtom) * kBK * kRowBytes);
       const uint32_t tx_dw = static_cast<uint32_t>(dw_a_bytes + (W.BN / kAtom) * dw_box);
       int stage = 0;
       uint32_t phase = 0;
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1u);
             uint8_t* sA = smem + stage * a.stage_bytes;
-            uint8_t* sB = sA + kStageABytes;
+            uint8_t* sB = sA + dx_a_bytes;
             mbar_arrive_expect_tx(&full[stage], tx_dx);
             tma_load_2d(sA, &tmGx, &full[stage], kb * kBK, mb * kBM);
             for (int j = 0; j < X.BN / kAtom; ++j)
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tc_fence_after();
           const uint32_t aS = smem_u32(smem + stage * a.stage_bytes);
           if (is_dx) {
-            const uint32_t bS = aS + kStageABytes;
+            const uint32_t bS = aS + a.dx.a_rows * kRowBytes;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t ad = umma_sdesc(aS + k * 32, 16, 1024);

@@ -82,7 +82,7 @@ struct F1Args {
 
 // Debug timeline (CTA 0): [period][16] globaltimer stamps, see splitfc_fwd_dx_kernel.
 __device__ unsigned long long g_f1_ts[64 * 16];
-__device__ unsigned long long g_f1_cta[160 * 3];  // per-CTA [entry, after prologue, end] (debug bit 0)
+__device__ unsigned long long g_f1_cta[160 * 5];  // per-CTA [entry, after prologue, end, after cluster sync, thread 0 at exit sync] (debug bit 0)
 
 __host__ __device__ constexpr int f1_smem_bytes(int stages, int s2) {
   return 1024 + stages * kF1G1SlotBytes + s2 * kF1G2SlotBytes + (kF1KC - 1) * kF1SlotBytes + 2 * kF1PBytes + 256;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
   const int ncl = static_cast<int>(ncluster_x());
   const int my_tiles = cl < a.num_tiles ? (a.num_tiles - 1 - cl) / ncl + 1 : 0;
   const uint32_t ucol0 = 3 * kF1NB;  // TMEM: Z buffers at 0, 32, 64; U blocks from 96
-  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) g_f1_cta[blockIdx.x * 3] = gtime_ns();
+  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) g_f1_cta[blockIdx.x * 5] = gtime_ns();
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S1; ++i) {
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
   TraceScope _trace(1);
   const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;
   const int d0 = static_cast<int>(q) * a.Dq;  // first feature column of this CTA's part
-  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) g_f1_cta[blockIdx.x * 3 + 1] = gtime_ns();
+  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) g_f1_cta[blockIdx.x * 5 + 1] = gtime_ns();
 
   // Schedule: G1 of tile p streams through ring 1 (from HBM); G2 of tile p - 1 re-reads its
   // W part through ring 2 (from L2, one period after G1 brought it in); the MMA issuer
@@ -588,7 +588,8 @@ __global__ void __launch_bounds__(kF1Threads, 1)
       named_bar_sync(2, kE);  // red_v is reused by the next tile
       if (dbg) g_f1_ts[it * 16 + 6] = gtime_ns();
     }
-    // ---- this CTA's part of U (relative to s_ref) -> global partials
+    // ---- this CTA's part of U (relative to s_ref) -> global partials (lanes: consecutive d,
+    //      128-byte warp stores; staging the 128 KB in smem for 1-D bulk copies measured slower)
     const size_t ubase = static_cast<size_t>(cl) * a.Bt;
     if (my_tiles > 0) {
       mbar_wait(&pempty[(my_tiles - 1) & 1], ((my_tiles - 1) >> 1) & 1);
@@ -610,14 +611,31 @@ __global__ void __launch_bounds__(kF1Threads, 1)
     }
     if (q == 0 && et < a.Bt) a.uref[ubase + et] = s_ref[et];
     if (et == 0) bulk_wait<0>();
+    if (a.debug & 32) __threadfence();  // timing experiment: drain the stores before the end stamp
+    // the peers' last remote operation on this CTA's shared memory is their "consumed"
+    // arrive for the last tile's partial: once it has landed nothing targets this CTA
+    if (my_tiles > 0) mbar_wait(xempty, (my_tiles - 1) & 1);
   }
+  // debug timeline: the exit stamps are kept in registers and stored together at the end (a
+  // store between two timer reads would time its own issue stall)
+  const unsigned long long t_pre = (a.debug & 1) ? gtime_ns() : 0ull;
   tc_fence_before();
   __syncthreads();
-  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) g_f1_cta[blockIdx.x * 3 + 2] = gtime_ns();
-  cluster_sync();  // no CTA leaves while a peer may still write into its shared memory
+  const unsigned long long t_end = (a.debug & 1) ? gtime_ns() : 0ull;
+  // no CTA leaves while a peer may still write into its shared memory: every remote write
+  // into this CTA was awaited above (Z partials via xfull, the consumed arrives via xempty),
+  // so the exit barrier orders nothing else and needs no release (no MEMBAR: the .release
+  // form waited ~12 us for the U write-out to drain)
+  if (!(a.debug & 64)) cluster_sync_relaxed();
+  const unsigned long long t_sync = (a.debug & 1) ? gtime_ns() : 0ull;
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, kF1TmemCols);
+  }
+  if ((a.debug & 1) && threadIdx.x == 0 && blockIdx.x < 160) {
+    g_f1_cta[blockIdx.x * 5 + 2] = t_end;
+    g_f1_cta[blockIdx.x * 5 + 3] = t_sync;
+    g_f1_cta[blockIdx.x * 5 + 4] = t_pre;  // thread 0 (TMA producer) reached the exit sync
   }
 }
 

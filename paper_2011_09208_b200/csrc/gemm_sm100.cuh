@@ -61,6 +61,12 @@ struct GemmArgs {
   int epi_bufs;             // smem store buffers per epilogue warp (2, 4 or 8)
   int bk;                   // K elements per stage: 128/ES, or 32 (bf16) when both operands are
                             // MN-major and K is short (dW at small B_tot)
+  int a_rows;               // K-major A: rows per TMA box = per smem A stage (kBM, or M rounded
+                            // up to 8 when all of M fits one block -- the B_tot-row operands at
+                            // small B_tot: no zero-filled rows take smem or TMA time, and the
+                            // freed bytes buy pipeline depth).  The M = 128 MMA still reads 128
+                            // rows: rows >= a_rows read whatever follows in smem, and their
+                            // accumulator rows (>= M) are never stored or used.
   // EPI_FWD_STATS
   const int32_t* labels;    // [M] global class ids
   long long class_offset;   // first class of this shard
@@ -516,7 +522,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
       uint32_t phase = 0;
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
       const int box_bytes = bk * kRowBytes;
-      const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
+      const int a_bytes = A_MN ? (kBM / kAtom) * box_bytes : a.a_rows * kRowBytes;
       // pairs: this CTA's half of B; the leader expects both CTAs' bytes
       const int bn_cta = a.BN / cs;
       const uint32_t tx = static_cast<uint32_t>(cs) *
@@ -583,7 +589,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
       const uint32_t idesc = umma_idesc(kBM * cs, a.BN, A_MN, B_MN, ES == 2 ? 1u : 2u);
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
       const uint32_t box_bytes = bk * kRowBytes;
-      const uint32_t a_bytes = A_MN ? (kBM / kAtom) * box_bytes : kStageABytes;
+      const uint32_t a_bytes = A_MN ? (kBM / kAtom) * box_bytes : a.a_rows * kRowBytes;
       const int kmma = bk / (32 / ES);  // MMAs (32 bytes of K each) per stage
       int stage = 0;
       uint32_t phase = 0;

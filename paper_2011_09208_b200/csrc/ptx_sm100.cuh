@@ -244,6 +244,12 @@ __device__ __forceinline__ uint32_t ncluster_x() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Cluster barrier without release semantics: no MEMBAR, so it does not wait for this
+// thread's outstanding global stores (F1's exit barrier took ~12 us with .release while the
+// CTA's U write-out drained).  Use only where nothing but the barrier itself is ordered.
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 // TMA load multicast to the same smem offset (and mbarrier offset) of every CTA in `mask`.
 __device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* map, uint64_t* bar, int c0, int c1,
                                                uint16_t mask) {

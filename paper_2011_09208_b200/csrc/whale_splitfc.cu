@@ -160,6 +160,7 @@ struct GemmCfg {
   int BN = 0, bk = 64, m_blocks = 0, n_blocks = 0, splits = 1, num_kb = 0, kb_per_split = 0, num_tiles = 0;
   int stages = 0, stage_bytes = 0, epi_bufs = 2, smem = 0, grid = 0;
   int cluster = 1;  // 2: CTA pairs share (TMA-multicast) the B tile of M-adjacent tiles
+  int a_rows = 128;  // K-major A rows per TMA box / smem stage (GemmArgs::a_rows)
 };
 
 static int env_int(const char* name, int dflt);
@@ -238,7 +239,7 @@ static void finish_cfg(GemmCfg& g, int sms, bool store_heavy, int es = 2, bool b
     const int atom = kRowBytes / es;
     g.stage_bytes = (kBM / atom + g.BN / atom) * g.bk * kRowBytes;
   } else {
-    g.stage_bytes = kStageABytes + g.BN * kRowBytes;
+    g.stage_bytes = g.a_rows * kRowBytes + g.BN * kRowBytes;
   }
   g.epi_bufs = store_heavy ? 8 : 2;
   const int avail = kSmemLimit - kStaticSmemSlack - 1024 - 256 - 4 * g.epi_bufs * kEpiBufBytes;
@@ -377,6 +378,17 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
     finish_cfg(p.dw, sms, p.dw.num_kb <= 4, p.es, p.es == 2);
   }
   p.dx = choose_splitk(p.Bt, p.D, p.Cr, atom, kbk, sms);
+  // the B_tot-row operands (X for the logits, G for dX): when all of B_tot fits one M block,
+  // load only its rows rounded up to 8 (one SW128 atom) -- at B_tot = 64 (c2, N = 2) a stage
+  // shrinks from 40 to 32 KB and the ring deepens from 4 to 6 stages
+  auto shrink_a = [&](GemmCfg& g, bool store_heavy) {
+    if (g.m_blocks == 1 && g.cluster == 1 && p.Bt < kBM && env_int("WHALE_SHRINK_A", 1) != 0) {
+      g.a_rows = static_cast<int>(align_up(p.Bt, 8));
+      finish_cfg(g, sms, store_heavy);
+    }
+  };
+  shrink_a(p.fwd, p.fwd.num_kb <= 4);  // as choose_plain
+  shrink_a(p.dx, false);               // as choose_splitk
   {
     const char* e = getenv("WHALE_F1");
     p.f1 = p.es == 2 && p.Bt <= kF1NB && p.D % (kF1KC * 128) == 0 && p.D / kF1KC <= 1024 &&
@@ -676,6 +688,7 @@ static GemmArgs base_args(const GemmCfg& g, int M, int N) {
   a.stage_bytes = g.stage_bytes;
   a.epi_bufs = g.epi_bufs;
   a.bk = g.bk;
+  a.a_rows = g.a_rows;
   a.store_mode = g_store_mode;
   a.n_fastest = g_n_fastest;
   a.debug = g_epi_debug;
@@ -845,7 +858,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   if (p.world > 1) {
     {
       const void* xg = c->symm[p.rank] + p.L.xg;
-      MAP_TRY(map2d(&c->tmX_fwd, xg, es, p.D, p.Bt, p.D * es, kbk, kBM));
+      MAP_TRY(map2d(&c->tmX_fwd, xg, es, p.D, p.Bt, p.D * es, kbk, p.fwd.a_rows));
       MAP_TRY(map2d(&c->tmX_dw, xg, es, p.D, p.Bt, p.D * es, atom, p.dw.bk));
       if (p.f1) MAP_TRY(map2d(&c->tmX_f1, xg, es, p.D, p.Bt, p.D * es, 64, kF1NB));
     }
@@ -853,7 +866,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   void* P = c->ws + p.L.P;
   MAP_TRY(map2d(&c->tmP_store, P, es, p.Cr, p.Bt, p.ldp * es, kRowBytes / es, 32));
   if (p.f1) MAP_TRY(map2d(&c->tmP_f1, P, es, p.Cr, p.Bt, p.ldp * es, 64, kF1NB));
-  MAP_TRY(map2d(&c->tmG_dx, P, es, p.Cr, p.Bt, p.ldp * es, kbk, kBM));
+  MAP_TRY(map2d(&c->tmG_dx, P, es, p.Cr, p.Bt, p.ldp * es, kbk, p.dx.a_rows));
   MAP_TRY(map2d(&c->tmG_dw, P, es, p.Cr, p.Bt, p.ldp * es, atom, p.dw.bk));
   MAP_TRY(map3d_out(&c->tmDxPart, c->ws + p.L.dxpart, p.D, p.Bt, p.dx.splits));
   if (es == 4) {
@@ -904,7 +917,7 @@ static whale_status_t ensure_x_maps(whale_splitfc_ctx* c, const void* x) {
   if (x == c->x_cached) return WHALE_OK;
   const Plan& p = c->p;
   const int kbk = kRowBytes / p.es, atom = kRowBytes / p.es;
-  whale_status_t st = map2d(&c->tmX_fwd, x, p.es, p.D, p.Bt, p.D * p.es, kbk, kBM);
+  whale_status_t st = map2d(&c->tmX_fwd, x, p.es, p.D, p.Bt, p.D * p.es, kbk, p.fwd.a_rows);
   if (st != WHALE_OK) return st;
   st = map2d(&c->tmX_dw, x, p.es, p.D, p.Bt, p.D * p.es, atom, p.dw.bk);
   if (st != WHALE_OK) return st;
@@ -1514,7 +1527,8 @@ extern "C" int whale_debug_f1_max_clusters(int smem) {
   return n;
 }
 
-// Internal: read the F1 debug timeline (64 periods x 16 stamps, then 160 CTAs x {entry, start, end}, ns).  Synchronises the device.
+// Internal: read the F1 debug timeline (64 periods x 16 stamps, then 160 CTAs x {entry, start, end,
+// after cluster sync, exit}, ns).  Synchronises the device.
 extern "C" int whale_debug_f1_timeline(unsigned long long* out) {
   if (cudaDeviceSynchronize() != cudaSuccess) return -1;
   if (cudaMemcpyFromSymbol(out, g_f1_ts, sizeof(g_f1_ts)) != cudaSuccess) return -2;

@@ -15,7 +15,7 @@ dx = torch.empty(B, D, dtype=torch.bfloat16, device="cuda"); dw = torch.empty(C,
 for _ in range(4):
     op.forward(X, y, W); op.backward(W, dx, dw)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (1024 + 480))()
+buf = (ctypes.c_ulonglong * (1024 + 800))()
 L.whale_debug_f1_timeline(buf)
 t0 = min(buf[p * 16 + k] for p in range(64) for k in (0, 7) if buf[p * 16 + k])
 names = ["mma_start", "g1_done", "mma_end", "epi_zfull", "epi_xfull", "epi_pfull", "epi_end", "prod_start",
@@ -24,9 +24,9 @@ print("period " + " ".join(n.rjust(9) for n in names))
 for p in range(14):
     print(str(p).rjust(6), " ".join(("%9.2f" % ((buf[p * 16 + k] - t0) / 1e3)) if buf[p * 16 + k] else " " * 9 for k in range(12)))
 
-ent = [buf[1024 + 3 * c] for c in range(148)]
-st = [buf[1024 + 3 * c + 1] for c in range(148)]
-en = [buf[1024 + 3 * c + 2] for c in range(148)]
+ent = [buf[1024 + 5 * c] for c in range(148)]
+st = [buf[1024 + 5 * c + 1] for c in range(148)]
+en = [buf[1024 + 5 * c + 2] for c in range(148)]
 g0 = min(st)
 print("CTA entry: min %.2f max %.2f us rel. first post-prologue stamp; prologue max %.2f us" % (
     (min(ent) - g0) / 1e3, (max(ent) - g0) / 1e3, max((b - a) / 1e3 for a, b in zip(ent, st))))

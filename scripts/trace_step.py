@@ -18,6 +18,9 @@ rank = int(os.environ.get("RANK", "0"))
 local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local); dev = torch.device("cuda", local)
 cfg = syn.CONFIGS[os.environ.get("CFG", "c2")]
+if os.environ.get("B") or os.environ.get("C"):  # shape overrides (e.g. one rank's shard shape at N = 1)
+    import dataclasses
+    cfg = dataclasses.replace(cfg, B=int(os.environ.get("B", cfg.B)), C=int(os.environ.get("C", cfg.C)))
 op = SplitFCSoftmaxCE(cfg.C, cfg.D, cfg.B, capacity=cfg.capacity, dtype=syn.torch_dtype(cfg.dtype), group=group, device=dev)
 X = syn.gen_features((rank * cfg.B, (rank + 1) * cfg.B), cfg.D, 1, cfg.dtype, device=dev)
 y = syn.gen_labels((rank * cfg.B, (rank + 1) * cfg.B), cfg.C, 1, device=dev).to(torch.int32)
@@ -58,6 +61,20 @@ for it in range(int(os.environ.get("ITERS", "5"))):
               "rowLast_lastchunk": [round((st[21 + j] - t0) / 1e3, 1) for j in range(2) if st[21 + j] >= t0]}
     out.append({"rank": rank, "it": it, "span_us": tend, "win_us": rec, "stats_stamps": stamps})
 L.whale_debug_trace_enable(0)
+if os.environ.get("WHALE_F1_DBG"):  # F1 per-CTA [entry, after prologue, end] of the last replay
+    tl = (ctypes.c_ulonglong * (1024 + 800))()
+    L.whale_debug_f1_timeline(tl)
+    ent = [tl[1024 + 5 * c] for c in range(148)]
+    en = [tl[1024 + 5 * c + 2] for c in range(148)]
+    cs = [tl[1024 + 5 * c + 3] for c in range(148)]
+    ex = [tl[1024 + 5 * c + 4] for c in range(148)]
+    span = lambda v: [round((min(v) - t0) / 1e3, 1), round((max(v) - t0) / 1e3, 1)]
+    if all(ent):
+        print(json.dumps({"rank": rank, "f1_cta_entry_us": span(ent), "f1_cta_end_us": span(en),
+                          "f1_after_cluster_sync_us": span(cs), "f1_t0_at_exit_sync_us": span(ex)}))
+        if os.environ.get("F1_CTA_DUMP"):
+            rel = lambda v: [round((x - t0) / 1e3, 2) for x in v]
+            json.dump({"entry": rel(ent), "end": rel(en), "sync": rel(cs), "exit": rel(ex)}, open(os.environ["F1_CTA_DUMP"], "w"))
 op.check()
 if group is not None:
     allo = [None] * world
