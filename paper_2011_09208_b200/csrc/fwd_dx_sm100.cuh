@@ -74,6 +74,8 @@ struct F1Args {
   const uint32_t* wait_flags;  // N > 1: gather flags (as GemmArgs)
   int wait_count;
   uint32_t wait_mult;
+  int gather_on;           // N > 1: the bridge all-gather fused into the prologue (as GemmArgs)
+  GatherArgs gather;
   uint32_t* dev_epoch;
   int* err;
   int debug;               // timing experiments: bit 0 = record a per-period timeline of CTA 0,
@@ -196,10 +198,17 @@ __global__ void __launch_bounds__(kF1Threads, 1)
   if (warp == 0 || warp == 3) {
     // ===================== TMA producers: warp 0 -> ring 1 (G1), warp 3 -> ring 2 (G2) =====
     if (lane == 0) {
-      if (a.wait_flags != nullptr) {
+      // only ring 1 carries X (the gathered rows); ring 2 re-reads the local W_r.  Fused gather:
+      // the first S1 slots get their W chunk at once and their X chunk after the wait.
+      bool x_ready = warp == 3 || a.wait_flags == nullptr;
+      auto wait_gathered = [&]() {
         for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
         fence_proxy_async_global();
-      }
+        x_ready = true;
+      };
+      if (!x_ready && !a.gather_on) wait_gathered();
+      int ndef = 0;
+      int def_slot[8], def_k[8];
       // L2 policy: G1 reads keep their lines (evict_last) until G2 re-reads them two periods
       // later (evict_first: last use), so DRAM sees W_r once
       const uint64_t keep = l2_policy_evict_last(), drop = l2_policy_evict_first();
@@ -211,16 +220,32 @@ __global__ void __launch_bounds__(kF1Threads, 1)
           if (dbg && it < 64) g_f1_ts[it * 16 + 7] = gtime_ns();
           const int row0 = (cl + it * ncl) * kF1TileC;
           for (int k = 0; k < KQ; ++k) {
+            if (!x_ready && ndef == S1) {  // ring full of slots waiting for X: the gathered rows
+              wait_gathered();
+              for (int i = 0; i < ndef; ++i)
+                tma_load_2d(ring1 + def_slot[i] * kF1G1SlotBytes + kF1StageBytes, &tmX, &full1[def_slot[i]], d0 + def_k[i] * 64, 0);
+            }
             mbar_wait(&empty1[stage], phase ^ 1u);
             uint8_t* slot = ring1 + stage * kF1G1SlotBytes;
             mbar_arrive_expect_tx(&full1[stage], kF1StageBytes + kF1XChunkBytes);
             tma_load_2d_hint(slot, &tmW, &full1[stage], d0 + k * 64, row0, keep);
-            tma_load_2d(slot + kF1StageBytes, &tmX, &full1[stage], d0 + k * 64, 0);
+            if (x_ready) {
+              tma_load_2d(slot + kF1StageBytes, &tmX, &full1[stage], d0 + k * 64, 0);
+            } else {
+              def_slot[ndef] = stage;
+              def_k[ndef] = k;
+              ++ndef;
+            }
             if (++stage == S1) {
               stage = 0;
               phase ^= 1u;
             }
           }
+        }
+        if (!x_ready) {  // fewer chunks than slots
+          wait_gathered();
+          for (int i = 0; i < ndef; ++i)
+            tma_load_2d(ring1 + def_slot[i] * kF1G1SlotBytes + kF1StageBytes, &tmX, &full1[def_slot[i]], d0 + def_k[i] * 64, 0);
         }
       } else if (!WHALE_SKIP(a.debug & 2)) {  // debug bit 2: timing experiment without G2
         for (int it = 0; it < my_tiles; ++it) {
@@ -380,6 +405,13 @@ __global__ void __launch_bounds__(kF1Threads, 1)
     const bool store_role = (qd % kF1KC) == static_cast<int>(q);  // one CTA stores each class row
     constexpr float kL2e = 1.4426950408889634f;
     constexpr int kE = kF1EpiThreads;
+    if (a.gather_on) {  // the fused bridge all-gather: this CTA's pieces, then one signal
+      int n = 0;
+      for (int part = static_cast<int>(blockIdx.x); part < a.gather.parts; part += static_cast<int>(gridDim.x), ++n)
+        gather_copy(a.gather, part, et, kE);
+      named_bar_sync(2, kE);
+      if (et == 0 && n > 0) gather_signal(a.gather, n);
+    }
     // N > 1: the gathered labels were stored by the peers' bridge_gather (generic stores +
     // fence.sc.sys + flag increments): acquire those flags before reading them (the producer
     // lanes' acquire does not order this thread's loads); the CTA barrier then orders the

@@ -79,6 +79,12 @@ struct GemmArgs {
   const uint32_t* wait_flags;  // [wait_count] local flag words, NULL = no wait
   int wait_count;
   uint32_t wait_mult;       // wait until flag >= epoch * wait_mult (monotonic counters)
+  // EPI_FWD_STATS at N > 1: the bridge all-gather fused into this kernel (gather_on = 1): the
+  // epilogue warps run the gather pieces blockIdx.x, blockIdx.x + gridDim.x, ... before their
+  // first tile, and the producer issues the B (W_r) loads of the first ring stages before it
+  // waits for the gathered A rows -- the W stream overlaps the NVLink exchange
+  int gather_on;
+  GatherArgs gather;
   // step epoch: every kernel reads e = *dev_epoch + 1 (device-resident, so a whole step can
   // be captured once in a CUDA graph and replayed); the last backward kernel bumps it
   uint32_t* dev_epoch;
@@ -512,12 +518,25 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (lane == 0) {
-      if (a.wait_flags != nullptr) {
-        // peers' rows of A were pushed over NVLink by generic-proxy stores; acquire their
-        // flags, then order the async-proxy (TMA) reads after them.
+      // peers' rows of A were pushed over NVLink by generic-proxy stores; acquire their
+      // flags, then order the async-proxy (TMA) reads after them.  With the fused gather (K-major
+      // A, no pairs) the first ring stages get their B loads at once and their A loads after
+      // the wait (deferred), so W_r streams while the all-gather lands.
+      bool a_ready = a.wait_flags == nullptr;
+      const bool defer = !a_ready && a.gather_on && !PAIR && !A_MN;
+      auto wait_gathered = [&]() {
         for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
         fence_proxy_async_global();
-      }
+        a_ready = true;
+      };
+      if (!a_ready && !defer) wait_gathered();
+      int ndef = 0;
+      int def_stage[8], def_kb[8], def_mb[8];
+      auto resolve = [&]() {  // gathered rows landed: the deferred A loads
+        wait_gathered();
+        for (int i = 0; i < ndef; ++i)
+          tma_load_2d(smem + def_stage[i] * a.stage_bytes, &tmA, &full[def_stage[i]], def_kb[i] * kBK, def_mb[i] * kBM);
+      };
       int stage = 0;
       uint32_t phase = 0;
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
@@ -532,10 +551,10 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
         int mb, nb, sp, kb0, kb1;
         decode_unit(a, tile, crank, mb, nb, sp, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* sA = smem + stage * a.stage_bytes;
           uint8_t* sB = sA + a_bytes;
           if constexpr (PAIR) {
+            mbar_wait(&empty[stage], phase ^ 1u);
             // pair: both CTAs load their own A rows and their half of B into their own smem;
             // the bytes complete on the leader's full barrier, which the leader alone arms
             const uint32_t fl = mapa_smem(smem_u32(&full[stage]), 0);
@@ -560,9 +579,16 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
             }
             continue;
           }
+          if (!a_ready && ndef == a.stages) resolve();  // (before waiting on a deferred stage)
+          mbar_wait(&empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full[stage], tx);
           if (WHALE_SKIP(a.debug & 8)) {
             // timing experiment: A operand not loaded
+          } else if (!a_ready) {
+            def_stage[ndef] = stage;  // A after the all-gather (K-major A only)
+            def_kb[ndef] = kb;
+            def_mb[ndef] = mb;
+            ++ndef;
           } else if (!A_MN) {
             tma_load_2d(sA, &tmA, &full[stage], kb * kBK, mb * kBM);
           } else {
@@ -582,6 +608,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
           }
         }
       }
+      if (!a_ready) resolve();  // fewer k-blocks than ring stages (or no tile)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (pairs: the leader only, M = 256) =====================
@@ -638,6 +665,13 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
     }
   } else if (EPI == EPI_FWD_STATS && warp >= 4) {
     // ===================== logits epilogue: 8 warps, 2 column groups =====================
+    if (a.gather_on) {  // the fused bridge all-gather: this CTA's pieces, then one signal
+      int n = 0;
+      for (int part = static_cast<int>(blockIdx.x); part < a.gather.parts; part += static_cast<int>(gridDim.x), ++n)
+        gather_copy(a.gather, part, threadIdx.x - 128, 256);
+      named_bar_sync(2, 256);
+      if (threadIdx.x == 128 && n > 0) gather_signal(a.gather, n);
+    }
     // N > 1: the gathered labels are peer-written (bridge_gather); acquire the gather flags
     // here too before any label read (the producer's acquire orders only its own lane)
     if (a.wait_flags != nullptr && threadIdx.x == 128)

@@ -60,61 +60,23 @@ __device__ __forceinline__ bool last_of_n(unsigned* counter, unsigned n) {
 }
 
 // ---------------------------------------------------------------- A2 bridge gather
-// Rank r writes its B_r rows at row offset R_r = B_0 + ... + B_{r-1} of every rank's gathered
-// X buffer (the concatenation in rank order), and its labels likewise; every block then
-// raises flag[GATHER][r] on every peer (B_r may be 0: the blocks still signal).
-// NVLS (mc_x != NULL): one multimem store per 16 bytes reaches every rank's gathered buffer
-// through the NVSwitch, and one multimem reduction raises flag[GATHER][r] on every rank.
-__global__ void bridge_gather_kernel(const uint4* __restrict__ x_local, const int32_t* __restrict__ y_local,
-                                     int64_t x_vecs /*B_r*row_bytes/16*/, int B, int row_off /*R_r*/,
-                                     int64_t row_vecs /*row_bytes/16*/, int rank, int world,
-                                     PeerPtrs dst_x /*slab base on each rank*/, PeerPtrs dst_y,
-                                     PeerFlags flags /*&flag[GATHER][rank] on each rank*/, int dbg,
-                                     uint4* mc_x /*multicast slab base or NULL*/, int32_t* mc_y, uint32_t* mc_flag) {
+// Stand-alone form of the bridge all-gather (used when it is not fused into the logits / F1
+// prologue, WHALE_FUSED_GATHER=0): block j runs piece j (gather_copy / gather_signal).
+// dbg & 16: globaltimer stamps of the first and last block (scripts/gather_ts.py).
+__global__ void bridge_gather_kernel(const GatherArgs g, int dbg) {
   const bool ts = (dbg & 16) && threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1);
   const int tso = blockIdx.x == 0 ? 0 : 8;
   if (ts) g_dbg_ts[tso + 0] = globaltimer();
-  if (!WHALE_SKIP(dbg & 4)) pdl_wait();
+  pdl_wait();
   pdl_trigger();
   TraceScope _trace(0);
   if (ts) g_dbg_ts[tso + 1] = globaltimer();
-  const int64_t off_vec = static_cast<int64_t>(row_off) * row_vecs;
-  if (mc_x != nullptr) {
-    for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < x_vecs;
-         v += static_cast<int64_t>(gridDim.x) * blockDim.x)
-      multimem_st_v4(mc_x + off_vec + v, __ldg(x_local + v));
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x)
-      multimem_st_u32(mc_y + row_off + i, static_cast<uint32_t>(y_local[i]));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence_system();  // orders the CTA's multimem stores (after the barrier) before the flag
-      if (dbg & 32) multimem_red_add_release_u32(mc_flag, 1u);
-      else multimem_red_add_relaxed_u32(mc_flag, 1u);  // flag[GATHER][rank] += 1 on every rank
-    }
-    return;
-  }
-  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < x_vecs;
-       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint4 val = __ldg(x_local + v);
-#pragma unroll
-    for (int p = 0; p < kMaxRanks; ++p)
-      if (p < world && (!WHALE_SKIP(dbg & 1) || p == rank)) reinterpret_cast<uint4*>(dst_x.p[p])[off_vec + v] = val;
-  }
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x) {
-    const int32_t y = y_local[i];
-#pragma unroll
-    for (int p = 0; p < kMaxRanks; ++p)
-      if (p < world) reinterpret_cast<int32_t*>(dst_y.p[p])[row_off + i] = y;
-  }
-  // every block signals every peer itself (no last-block ticket): after the CTA barrier,
-  // one fence.sc.sys + a relaxed increment per peer; peers wait for epoch * gridDim.x.
+  gather_copy(g, blockIdx.x, threadIdx.x, blockDim.x);
   if (ts) g_dbg_ts[tso + 2] = globaltimer();
   __syncthreads();
   if (ts) g_dbg_ts[tso + 3] = globaltimer();
   if (threadIdx.x == 0) {
-    if (!WHALE_SKIP(dbg & 2)) __threadfence_system();
-    if (ts) g_dbg_ts[tso + 4] = globaltimer();
-    for (int p = 0; p < world; ++p) red_add_relaxed_sys(flags.p[p], 1u);  // ordered by the fence
+    gather_signal(g, 1);
     if (ts) g_dbg_ts[tso + 5] = globaltimer();
   }
 }

@@ -561,4 +561,65 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
+// ------------------------------------------------------------------ A2 bridge all-gather parts
+// The bridge all-gather of the feature rows ("concatenation in batch
+// dimension") as `parts` equal pieces: piece j copies vectors [j*per, (j+1)*per) of this rank's
+// rows X_r (and its labels) to row offset R_r of every rank's gathered buffer, then raises
+// flag[GATHER][rank] by one on every rank.  A consumer waits for flag >= epoch * parts for
+// every source rank.  `parts` depends only on (B_max, D), so it is the same on every rank.
+// The pieces run either in the stand-alone bridge_gather_kernel (one block each) or in the
+// prologue of the kernel that consumes the gathered rows (the logits GEMM / F1), by its
+// otherwise idle epilogue warps -- the all-gather fused into the GEMM that reads it.
+struct GatherArgs {
+  const uint4* x_local;  // [B_r x D] rows of this rank (16-byte vectors)
+  const int32_t* y_local;
+  int64_t x_vecs;        // B_r * D * es / 16
+  int B;                 // B_r
+  int row_off;           // R_r
+  int64_t row_vecs;      // D * es / 16
+  int rank, world, parts;
+  PeerPtrs dst_x, dst_y;  // gathered X / y slab base on each rank
+  PeerFlags flags;        // &flag[GATHER][rank] on each rank
+  uint4* mc_x;            // NVLS multicast views (or NULL): one multimem op reaches every rank
+  int32_t* mc_y;
+  uint32_t* mc_flag;
+};
+
+// Piece `part` by `nthr` threads (thread index `t`); the caller then runs
+// gather_signal() from ONE of those threads after a barrier over all `nthr` of them.
+__device__ __forceinline__ void gather_copy(const GatherArgs& g, int part, int t, int nthr) {
+  const int64_t per = (g.x_vecs + g.parts - 1) / g.parts;
+  const int64_t v0 = static_cast<int64_t>(part) * per, v1 = v0 + per < g.x_vecs ? v0 + per : g.x_vecs;
+  const int64_t off_vec = static_cast<int64_t>(g.row_off) * g.row_vecs;
+  const int yper = (g.B + g.parts - 1) / g.parts;
+  const int y0 = part * yper, y1 = y0 + yper < g.B ? y0 + yper : g.B;
+  if (g.mc_x != nullptr) {
+    for (int64_t v = v0 + t; v < v1; v += nthr) multimem_st_v4(g.mc_x + off_vec + v, __ldg(g.x_local + v));
+    for (int i = y0 + t; i < y1; i += nthr) multimem_st_u32(g.mc_y + g.row_off + i, static_cast<uint32_t>(g.y_local[i]));
+    return;
+  }
+  for (int64_t v = v0 + t; v < v1; v += nthr) {
+    const uint4 val = __ldg(g.x_local + v);
+#pragma unroll
+    for (int p = 0; p < kMaxRanks; ++p)
+      if (p < g.world) reinterpret_cast<uint4*>(g.dst_x.p[p])[off_vec + v] = val;
+  }
+  for (int i = y0 + t; i < y1; i += nthr) {
+    const int32_t y = g.y_local[i];
+#pragma unroll
+    for (int p = 0; p < kMaxRanks; ++p)
+      if (p < g.world) reinterpret_cast<int32_t*>(g.dst_y.p[p])[g.row_off + i] = y;
+  }
+}
+// After a barrier over the copying threads: one fence.sc.sys orders all of their stores
+// (cumulativity through the barrier) before the relaxed flag increments.
+__device__ __forceinline__ void gather_signal(const GatherArgs& g, int npieces) {
+  __threadfence_system();
+  if (g.mc_x != nullptr) {
+    multimem_red_add_relaxed_u32(g.mc_flag, static_cast<uint32_t>(npieces));  // on every rank at once
+  } else {
+    for (int p = 0; p < g.world; ++p) red_add_relaxed_sys(g.flags.p[p], static_cast<uint32_t>(npieces));
+  }
+}
+
 }  // namespace whale

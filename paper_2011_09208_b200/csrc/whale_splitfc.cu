@@ -401,7 +401,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
       // real static shared memory
       p.f1_s2 = std::max(1, std::min(kF1S2Max, env_int("WHALE_F1_S2", 3)));
       const int fixed = f1_smem_bytes(0, p.f1_s2) + 2048;
-      p.f1_stages = std::min(env_int("WHALE_F1_S1", 8), (kSmemLimit - fixed) / kF1G1SlotBytes);
+      p.f1_stages = std::min(std::min(env_int("WHALE_F1_S1", 8), 8), (kSmemLimit - fixed) / kF1G1SlotBytes);
       p.f1_smem = f1_smem_bytes(p.f1_stages, p.f1_s2);
       if (p.f1_stages < 3) p.f1 = false;
     }
@@ -562,6 +562,7 @@ struct whale_splitfc_ctx {
   bool fused_bwd = true;             // dW + dX in one persistent launch (bf16)
   bool gfuse = true;                 // G-fused backward (NEXT-4b): G formed from P~ in the bwd operand path
   bool row_bulk = false;             // dW tiles stored as 1-D bulk row copies (bwd_sm100.cuh)
+  bool fused_gather = true;          // N > 1: bridge all-gather inside the logits / F1 prologue
   bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
@@ -793,6 +794,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     CUDA_TRY(cudaMemcpyToSymbol(g_wait_timeout_ns, &ns, sizeof(ns)));
   }
   c->fused_bwd = p.es == 2 && env_int("WHALE_FUSED_BWD", 1) != 0 && g_store_mode == 1;
+  c->fused_gather = env_int("WHALE_FUSED_GATHER", 1) != 0;
   c->gfuse = c->fused_bwd && env_int("WHALE_GFUSE", 0) != 0;
   if (p.dw_bf16 && !c->fused_bwd) {
     delete c;
@@ -826,7 +828,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     cudaFuncAttributes fa{};
     CUDA_TRY(cudaFuncGetAttributes(&fa, splitfc_fwd_dx_kernel));
     const int fixed = f1_smem_bytes(0, p.f1_s2) + static_cast<int>(fa.sharedSizeBytes);
-    c->p.f1_stages = std::min(env_int("WHALE_F1_S1", 8), (kSmemLimit - fixed) / kF1G1SlotBytes);
+    c->p.f1_stages = std::min(std::min(env_int("WHALE_F1_S1", 8), 8), (kSmemLimit - fixed) / kF1G1SlotBytes);
     c->p.f1_smem = f1_smem_bytes(c->p.f1_stages, p.f1_s2);
     if (c->p.f1_stages < 3) {
       delete c;
@@ -951,6 +953,8 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     if (st != WHALE_OK) return st;
   }
   const int32_t* yg;
+  GatherArgs gth{};
+  bool gather_fused = false;
   if (p.world == 1) {
     whale_status_t st = ensure_x_maps(c, x_local);
     if (st != WHALE_OK) return st;
@@ -958,25 +962,32 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     c->x_fwd = x_local;
     c->y_fwd = y_local;
   } else {
-    // ---- A2 bridge all-gather over NVLink
-    PeerPtrs dx{}, dy{};
-    PeerFlags fl{};
+    // ---- A2 bridge all-gather over NVLink: fused into the logits / F1 prologue (default), or
+    //      a kernel of its own (WHALE_FUSED_GATHER=0)
+    gth.x_local = static_cast<const uint4*>(x_local);
+    gth.y_local = y_local;
+    gth.x_vecs = p.B * p.D * ES / 16;
+    gth.B = static_cast<int>(p.B);
+    gth.row_off = static_cast<int>(p.Boff[p.rank]);
+    gth.row_vecs = p.D * ES / 16;
+    gth.rank = p.rank;
+    gth.world = p.world;
+    gth.parts = gather_grid(p);
     for (int r = 0; r < p.world; ++r) {
-      dx.p[r] = c->symm[r] + L.xg;
-      dy.p[r] = c->symm[r] + L.yg;
-      fl.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_GATHER * kMaxRanks + p.rank;
+      gth.dst_x.p[r] = c->symm[r] + L.xg;
+      gth.dst_y.p[r] = c->symm[r] + L.yg;
+      gth.flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_GATHER * kMaxRanks + p.rank;
+    }
+    if (c->mc) {
+      gth.mc_x = reinterpret_cast<uint4*>(c->mc + L.xg);
+      gth.mc_y = reinterpret_cast<int32_t*>(c->mc + L.yg);
+      gth.mc_flag = reinterpret_cast<uint32_t*>(c->mc + L.flags) + FLAG_GATHER * kMaxRanks + p.rank;
     }
     yg = reinterpret_cast<const int32_t*>(c->symm[p.rank] + L.yg);
-    const int64_t x_vecs = p.B * p.D * ES / 16;
-    const int grid = gather_grid(p);
-    PROFILED(K_GATHER, s,
-             (launch(c, bridge_gather_kernel, dim3(grid), dim3(256), 0, s, static_cast<const uint4*>(x_local),
-                     y_local, x_vecs, static_cast<int>(p.B), static_cast<int>(p.Boff[p.rank]),
-                     static_cast<int64_t>(p.D * ES / 16), p.rank, p.world, dx, dy, fl,
-                     env_int("WHALE_GATHER_DBG", 0),
-                     c->mc ? reinterpret_cast<uint4*>(c->mc + L.xg) : nullptr,
-                     c->mc ? reinterpret_cast<int32_t*>(c->mc + L.yg) : nullptr,
-                     c->mc ? reinterpret_cast<uint32_t*>(c->mc + L.flags) + FLAG_GATHER * kMaxRanks + p.rank : nullptr)));
+    gather_fused = c->fused_gather;
+    if (!gather_fused)
+      PROFILED(K_GATHER, s, (launch(c, bridge_gather_kernel, dim3(gth.parts), dim3(256), 0, s, gth,
+                                    env_int("WHALE_GATHER_DBG", 0))));
   }
   // ---- A3 logits GEMM with fused row statistics
   if (ES == 2 && p.f1) {
@@ -1007,6 +1018,8 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
       a.wait_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_GATHER * kMaxRanks;
       a.wait_count = p.world;
       a.wait_mult = static_cast<uint32_t>(gather_grid(p));
+      a.gather_on = gather_fused ? 1 : 0;
+      a.gather = gth;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.f1_ncl * kF1KC);
@@ -1040,7 +1053,9 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     if (p.world > 1) {
       a.wait_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_GATHER * kMaxRanks;
       a.wait_count = p.world;
-      a.wait_mult = static_cast<uint32_t>(gather_grid(p));  // one increment per gather block
+      a.wait_mult = static_cast<uint32_t>(gather_grid(p));  // one increment per gather piece
+      a.gather_on = gather_fused ? 1 : 0;
+      a.gather = gth;
     }
     PROFILED(K_LOGITS, s,
              (launch_gemm<EPI_FWD_STATS, false, false, ES>(c, ES == 2 ? 0 : 3, p.fwd, c->tmX_fwd,
@@ -1403,6 +1418,7 @@ extern "C" int32_t whale_splitfc_launches_per_step(const whale_splitfc_ctx* ctx)
   // N = 1: logits, stats+grad, dW, dX;  N > 1: + gather, + dX owner reduce
   int base = ctx->p.world == 1 ? 4 : 6;
   if (ctx->fused_bwd) base -= 1;  // dW + dX share one launch (F1: dW tiles + dX combine units)
+  if (ctx->p.world > 1 && ctx->fused_gather) base -= 1;  // the gather runs in the logits / F1 prologue
   // F1 unfused: the combine kernel replaces the dX GEMM (same count)
   return base + (ctx->p.es == 4 ? 3 : 0);  // fp32 path: operand transposes
 }
