@@ -178,7 +178,15 @@ constexpr int kSchedSlots = 4;
 
 // DWB: dW_r stored in bf16 (a separate instantiation, so the fp32 kernel carries none of the
 // bf16 store code and keeps its register allocation)
-template <int ES, bool DWB>
+// PAIR: CTA pairs (launched as 2-CTA clusters; tensor-bound shapes, e.g. c5): every unit is
+// an M = 256 tcgen05.mma.cta_group::2 tile over two M blocks -- each CTA loads its own 128 A
+// rows and HALF of the B tile (a stage costs 32 instead of 48 KB, and each SM's tensor core
+// reads half the B bytes), the leader's MMA thread issues for both, its commits multicast to
+// both CTAs, and each CTA's epilogue stores its own 128 rows.  The leader's producer runs the
+// dynamic scheduler and hands every unit id to the peer through distributed shared memory
+// (st.async into the peer's slot + complete_tx on its slot barrier).  Requires no split-K
+// (dx.splits == 1), no F1 combine units and no G-fused transformers.
+template <int ES, bool DWB, bool PAIR = false>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     splitfc_bwd_kernel(const __grid_constant__ CUtensorMap tmGx, const __grid_constant__ CUtensorMap tmW,
                        const __grid_constant__ CUtensorMap tmPart, const __grid_constant__ CUtensorMap tmGw,
@@ -205,20 +213,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int total = a.ux + a.tw + a.tc;
-  const bool xf = a.gf.gscale != nullptr;  // G-fused operand path
+  const bool xf = !PAIR && a.gf.gscale != nullptr;  // G-fused operand path
+  constexpr int cs = PAIR ? 2 : 1;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;
+  const int uid0 = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);  // first unit
+  const int nuid = PAIR ? static_cast<int>(ncluster_x()) : static_cast<int>(gridDim.x);   // units in flight
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < a.stages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&full[i], 1);   // pairs: the leader's expect_tx; both CTAs' TMA bytes land on the leader's
+      mbar_init(&empty[i], 1);  // pairs: the leader's multicast commit
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 128 * cs);  // pairs: both CTAs' epilogue threads, on the leader's
     }
     for (int i = 0; i < kSchedSlots; ++i) {
       mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], 1 + 4 + (xf ? 4 : 0));  // MMA thread + 4 epilogue warps (+ 4 transformer warps)
+      // MMA thread + 4 epilogue warps (+ 4 transformer warps); pairs: on the leader's, plus the
+      // peer's producer and 4 epilogue warps (the peer's MMA thread does not read the ring)
+      mbar_init(&sempty[i], 1 + 4 + (xf ? 4 : 0) + (PAIR ? 5 : 0));
     }
     for (int i = 0; i < a.stages; ++i) mbar_init(&ready[i], 4);
     fence_mbar_init();
@@ -231,7 +245,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tma_prefetch_desc(&tmX);
     tma_prefetch_desc(&tmDW);
   }
-  if (warp == 2) tmem_alloc(tmem_holder, kTmemCols);
+  if (PAIR) cluster_sync();  // peer barriers initialised before any remote arrive / TMA / st.async
+  if (warp == 2) {
+    if constexpr (PAIR) tmem_alloc_pair(tmem_holder, kTmemCols);
+    else tmem_alloc(tmem_holder, kTmemCols);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -239,6 +257,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   pdl_wait();
   pdl_trigger();
   TraceScope _trace(8);
+  // a consumer is done with scheduler slot `sl` (pairs: on the leader's barrier)
+  auto release_slot = [&](int sl) {
+    if (PAIR) mbar_arrive_remote(mapa_smem(smem_u32(&sempty[sl]), 0));
+    else mbar_arrive(&sempty[sl]);
+  };
+  // an epilogue thread's TMEM reads of accumulator `acc` are complete (tcgen05.wait::ld, fence
+  // issued): hand it back -- pairs: to the leader's MMA (relaxed: the loads already completed)
+  auto release_acc_bwd = [&](uint64_t* bar) {
+    if (PAIR) mbar_arrive_remote(mapa_smem(smem_u32(bar), 0));
+    else mbar_arrive(bar);
+  };
   const uint32_t e = ld_acquire_gpu(a.dx.dev_epoch) + 1u;  // this step's epoch
 
   if (warp == 0) {
@@ -250,49 +279,82 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int dw_box = dw_bk * kRowBytes;
       const int dw_a_bytes = (kBM / kAtom) * dw_box;
       const int dx_a_bytes = X.a_rows * kRowBytes;  // G rows per stage (B_tot rounded up to 8 when < 128)
-      const uint32_t tx_dx = static_cast<uint32_t>(dx_a_bytes + (X.BN / kAtom) * kBK * kRowBytes);
-      const uint32_t tx_dw = static_cast<uint32_t>(dw_a_bytes + (W.BN / kAtom) * dw_box);
+      // pairs: this CTA's half of each B tile; the leader's full barrier expects both CTAs' bytes
+      const int dx_bn = X.BN / cs, dw_bn = W.BN / cs;
+      const uint32_t tx_dx = static_cast<uint32_t>(cs * (dx_a_bytes + (dx_bn / kAtom) * kBK * kRowBytes));
+      const uint32_t tx_dw = static_cast<uint32_t>(cs * (dw_a_bytes + (dw_bn / kAtom) * dw_box));
       int stage = 0;
       uint32_t phase = 0;
-      int unit = blockIdx.x;
+      int unit = uid0;
       for (int it = 0;; ++it) {
         const int slot = it % kSchedSlots;
-        mbar_wait(&sempty[slot], ((it / kSchedSlots) & 1) ^ 1u);
-        if (it > 0) unit = static_cast<int>(atomicAdd(a.sched_cnt, 1u)) + gridDim.x;
-        if (unit >= total) unit = -1;
-        sched_tile[slot] = unit;
-        mbar_arrive(&sfull[slot]);
+        if (!PAIR || crank == 0) {
+          mbar_wait(&sempty[slot], ((it / kSchedSlots) & 1) ^ 1u);
+          if (it > 0) unit = static_cast<int>(atomicAdd(a.sched_cnt, 1u)) + nuid;
+          if (unit >= total) unit = -1;
+          sched_tile[slot] = unit;
+          mbar_arrive(&sfull[slot]);
+          if (PAIR) {  // hand the unit to the peer: 4 bytes into its slot, completing its barrier
+            const uint32_t pbar = mapa_smem(smem_u32(&sfull[slot]), 1);
+            mbar_arrive_expect_tx_remote(pbar, 4u);
+            st_async_u32(mapa_smem(smem_u32(&sched_tile[slot]), 1), pbar, static_cast<uint32_t>(unit));
+          }
+        } else {  // pair peer: the leader's unit
+          mbar_wait(&sfull[slot], (it / kSchedSlots) & 1);
+          unit = sched_tile[slot];
+          release_slot(slot);
+        }
         if (unit < 0) break;
         if (unit < a.tc) continue;  // combine unit: epilogue-only work
         unit -= a.tc;
         int mb, nb, sp, kb0, kb1;
         if (unit < a.ux) {
-          decode_tile(X, unit, mb, nb, sp, kb0, kb1);
+          decode_unit(X, unit, crank, mb, nb, sp, kb0, kb1);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1u);
             uint8_t* sA = smem + stage * a.stage_bytes;
             uint8_t* sB = sA + dx_a_bytes;
-            mbar_arrive_expect_tx(&full[stage], tx_dx);
-            tma_load_2d(sA, &tmGx, &full[stage], kb * kBK, mb * kBM);
-            for (int j = 0; j < X.BN / kAtom; ++j)
-              tma_load_2d(sB + j * kBK * kRowBytes, &tmW, &full[stage], nb * X.BN + j * kAtom, kb * kBK);
+            if constexpr (PAIR) {
+              const uint32_t fl = mapa_smem(smem_u32(&full[stage]), 0);
+              if (crank == 0) mbar_arrive_expect_tx(&full[stage], tx_dx);
+              tma_load_2d_pair(sA, &tmGx, fl, kb * kBK, mb * kBM);
+              for (int j = 0; j < dx_bn / kAtom; ++j)
+                tma_load_2d_pair(sB + j * kBK * kRowBytes, &tmW, fl, nb * X.BN + static_cast<int>(crank) * dx_bn + j * kAtom,
+                                 kb * kBK);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], tx_dx);
+              tma_load_2d(sA, &tmGx, &full[stage], kb * kBK, mb * kBM);
+              for (int j = 0; j < X.BN / kAtom; ++j)
+                tma_load_2d(sB + j * kBK * kRowBytes, &tmW, &full[stage], nb * X.BN + j * kAtom, kb * kBK);
+            }
             if (++stage == a.stages) {
               stage = 0;
               phase ^= 1u;
             }
           }
         } else {
-          decode_tile(W, unit - a.ux, mb, nb, sp, kb0, kb1);
+          decode_unit(W, unit - a.ux, crank, mb, nb, sp, kb0, kb1);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1u);
             uint8_t* sA = smem + stage * a.stage_bytes;
             uint8_t* sB = sA + dw_a_bytes;
-            mbar_arrive_expect_tx(&full[stage], tx_dw);
+            if constexpr (PAIR) {
+              const uint32_t fl = mapa_smem(smem_u32(&full[stage]), 0);
+              if (crank == 0) mbar_arrive_expect_tx(&full[stage], tx_dw);
 #pragma unroll
-            for (int j = 0; j < kBM / kAtom; ++j)
-              tma_load_2d(sA + j * dw_box, &tmGw, &full[stage], mb * kBM + j * kAtom, kb * dw_bk);
-            for (int j = 0; j < W.BN / kAtom; ++j)
-              tma_load_2d(sB + j * dw_box, &tmX, &full[stage], nb * W.BN + j * kAtom, kb * dw_bk);
+              for (int j = 0; j < kBM / kAtom; ++j)
+                tma_load_2d_pair(sA + j * dw_box, &tmGw, fl, mb * kBM + j * kAtom, kb * dw_bk);
+              for (int j = 0; j < dw_bn / kAtom; ++j)
+                tma_load_2d_pair(sB + j * dw_box, &tmX, fl, nb * W.BN + static_cast<int>(crank) * dw_bn + j * kAtom,
+                                 kb * dw_bk);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], tx_dw);
+#pragma unroll
+              for (int j = 0; j < kBM / kAtom; ++j)
+                tma_load_2d(sA + j * dw_box, &tmGw, &full[stage], mb * kBM + j * kAtom, kb * dw_bk);
+              for (int j = 0; j < W.BN / kAtom; ++j)
+                tma_load_2d(sB + j * dw_box, &tmX, &full[stage], nb * W.BN + j * kAtom, kb * dw_bk);
+            }
             if (++stage == a.stages) {
               stage = 0;
               phase ^= 1u;
@@ -302,10 +364,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      const uint32_t idesc_dx = umma_idesc(kBM, a.dx.BN, false, true, ES == 2 ? 1u : 2u);
-      const uint32_t idesc_dw = umma_idesc(kBM, a.dw.BN, true, true, ES == 2 ? 1u : 2u);
+    // ===================== MMA issuer (pairs: the leader only, M = 256) =====================
+    if (lane == 0 && crank == 0) {
+      const uint32_t idesc_dx = umma_idesc(kBM * cs, a.dx.BN, false, true, ES == 2 ? 1u : 2u);
+      const uint32_t idesc_dw = umma_idesc(kBM * cs, a.dw.BN, true, true, ES == 2 ? 1u : 2u);
       const uint32_t dw_box = a.dw.bk * kRowBytes;
       const uint32_t dw_a_bytes = (kBM / kAtom) * dw_box;
       const int dw_kmma = a.dw.bk / (32 / ES);
@@ -322,8 +384,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int gu = unit - a.tc;
         const bool is_dx = gu < a.ux;
         int mb, nb, sp, kb0, kb1;
-        if (is_dx) decode_tile(a.dx, gu, mb, nb, sp, kb0, kb1);
-        else decode_tile(a.dw, gu - a.ux, mb, nb, sp, kb0, kb1);
+        if (is_dx) decode_unit(a.dx, gu, 0u, mb, nb, sp, kb0, kb1);
+        else decode_unit(a.dw, gu - a.ux, 0u, mb, nb, sp, kb0, kb1);
         const int acc = na & 1;
         const uint32_t aph = (na >> 1) & 1;
         ++na;
@@ -340,23 +402,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             for (int k = 0; k < 4; ++k) {
               const uint64_t ad = umma_sdesc(aS + k * 32, 16, 1024);
               const uint64_t bd = umma_sdesc(bS + k * kKStepMN, kBK * kRowBytes, 1024);
-              umma_bf16(d_tmem, ad, bd, idesc_dx, (kb > kb0 || k > 0) ? 1u : 0u);
+              if constexpr (PAIR) umma_bf16_pair(d_tmem, ad, bd, idesc_dx, (kb > kb0 || k > 0) ? 1u : 0u);
+              else umma_bf16(d_tmem, ad, bd, idesc_dx, (kb > kb0 || k > 0) ? 1u : 0u);
             }
           } else {
             const uint32_t bS = aS + dw_a_bytes;
             for (int k = 0; k < dw_kmma; ++k) {
               const uint64_t ad = umma_sdesc(aS + k * kKStepMN, dw_box, 1024);
               const uint64_t bd = umma_sdesc(bS + k * kKStepMN, dw_box, 1024);
-              umma_bf16(d_tmem, ad, bd, idesc_dw, (kb > kb0 || k > 0) ? 1u : 0u);
+              if constexpr (PAIR) umma_bf16_pair(d_tmem, ad, bd, idesc_dw, (kb > kb0 || k > 0) ? 1u : 0u);
+              else umma_bf16(d_tmem, ad, bd, idesc_dw, (kb > kb0 || k > 0) ? 1u : 0u);
             }
           }
-          umma_commit(&empty[stage]);
+          if constexpr (PAIR) umma_commit_pair_mc(&empty[stage], 0x3);  // frees the stage in both CTAs
+          else umma_commit(&empty[stage]);
           if (++stage == a.stages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (PAIR) umma_commit_pair_mc(&tfull[acc], 0x3);  // both halves ready
+        else umma_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4 && warp < 8) {
@@ -370,7 +436,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(&sfull[slot], (it / kSchedSlots) & 1);
       const int unit = sched_tile[slot];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&sempty[slot]);
+      if (lane == 0) release_slot(slot);
       if (unit < 0) break;
       if (unit < a.tc) {
         combine_unit(a.cb, unit, s_fac);
@@ -380,7 +446,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const bool is_dx = gu < a.ux;
       const GemmArgs& g = is_dx ? a.dx : a.dw;
       int mb, nb, sp, kb0, kb1;
-      decode_tile(g, is_dx ? gu : gu - a.ux, mb, nb, sp, kb0, kb1);
+      decode_unit(g, is_dx ? gu : gu - a.ux, crank, mb, nb, sp, kb0, kb1);
       const CUtensorMap* om = is_dx ? &tmPart : &tmDW;
       const int acc = na & 1;
       const uint32_t aph = (na >> 1) & 1;
@@ -400,7 +466,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tmem_ld_wait();
           if (c0 + 32 >= g.BN) {
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            release_acc_bwd(&tempty[acc]);
           }
           if (a.dx.grad_scale) scale32(v, dws);
           if constexpr (DWB) {
@@ -437,7 +503,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tmem_ld_wait();
           if (c0 + 64 >= g.BN) {
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            release_acc_bwd(&tempty[acc]);
           }
           if (c0 + 32 >= g.BN) {
 #pragma unroll
@@ -472,7 +538,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_ld_wait();
         if (c0 + 32 >= g.BN) {
           tc_fence_before();
-          mbar_arrive(&tempty[acc]);
+          release_acc_bwd(&tempty[acc]);
         }
         if (!is_dx && a.dx.grad_scale) scale32(v, dws);
         if (threadIdx.x == 128) bulk_wait_read_n(nbuf);
@@ -616,9 +682,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  // pairs: the peer may still receive the leader's commits / send its arrives
+  if (PAIR) cluster_sync();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, kTmemCols);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem_base, kTmemCols);
+    else tmem_dealloc(tmem_base, kTmemCols);
   }
   end_of_step_ticket(a.dx, e, s_fix_go, a.sched_cnt);  // RS flags (N > 1) + epoch publish + counter reset
 }

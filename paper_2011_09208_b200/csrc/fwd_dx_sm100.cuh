@@ -87,7 +87,7 @@ __device__ unsigned long long g_f1_ts[64 * 16];
 __device__ unsigned long long g_f1_cta[160 * 5];  // per-CTA [entry, after prologue, end, after cluster sync, thread 0 at exit sync] (debug bit 0)
 
 __host__ __device__ constexpr int f1_smem_bytes(int stages, int s2) {
-  return 1024 + stages * kF1G1SlotBytes + s2 * kF1G2SlotBytes + (kF1KC - 1) * kF1SlotBytes + 2 * kF1PBytes + 256;
+  return 1024 + stages * kF1G1SlotBytes + s2 * kF1G2SlotBytes + (kF1KC - 1) * kF1SlotBytes + 2 * kF1PBytes + 512;
 }
 
 // Warp-wide fp32 max (sm_100a redux.sync .f32), result in every lane.
@@ -140,7 +140,8 @@ __global__ void __launch_bounds__(kF1Threads, 1)
   uint64_t* pempty = pfull + 2;      // completes when G2 of that buffer's tile finished
   uint64_t* xfull = pempty + 2;
   uint64_t* xempty = xfull + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xempty + 1);
+  uint64_t* ublk = xempty + 1;        // [KQ / 2 <= 8]: U block i final (the last tile's G2 block i done)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ublk + 8);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
     }
     mbar_init(xfull, 1);
     mbar_init(xempty, kF1KC - 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&ublk[i], 1);
     fence_mbar_init();
   }
   if (threadIdx.x == 32) {
@@ -200,15 +202,16 @@ __global__ void __launch_bounds__(kF1Threads, 1)
     if (lane == 0) {
       // only ring 1 carries X (the gathered rows); ring 2 re-reads the local W_r.  Fused gather:
       // the first S1 slots get their W chunk at once and their X chunk after the wait.
+      // (no lambdas / arrays here: captured or indexed locals would live in local memory and
+      // measurably slowed the issue loop; the deferred slots are simply slots 0 .. ndef - 1,
+      // and slot i's X chunk is chunk i % KQ)
       bool x_ready = warp == 3 || a.wait_flags == nullptr;
-      auto wait_gathered = [&]() {
+      if (!x_ready && !a.gather_on) {
         for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
         fence_proxy_async_global();
         x_ready = true;
-      };
-      if (!x_ready && !a.gather_on) wait_gathered();
+      }
       int ndef = 0;
-      int def_slot[8], def_k[8];
       // L2 policy: G1 reads keep their lines (evict_last) until G2 re-reads them two periods
       // later (evict_first: last use), so DRAM sees W_r once
       const uint64_t keep = l2_policy_evict_last(), drop = l2_policy_evict_first();
@@ -221,21 +224,18 @@ __global__ void __launch_bounds__(kF1Threads, 1)
           const int row0 = (cl + it * ncl) * kF1TileC;
           for (int k = 0; k < KQ; ++k) {
             if (!x_ready && ndef == S1) {  // ring full of slots waiting for X: the gathered rows
-              wait_gathered();
+              for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
+              fence_proxy_async_global();
+              x_ready = true;
               for (int i = 0; i < ndef; ++i)
-                tma_load_2d(ring1 + def_slot[i] * kF1G1SlotBytes + kF1StageBytes, &tmX, &full1[def_slot[i]], d0 + def_k[i] * 64, 0);
+                tma_load_2d(ring1 + i * kF1G1SlotBytes + kF1StageBytes, &tmX, &full1[i], d0 + (i % KQ) * 64, 0);
             }
             mbar_wait(&empty1[stage], phase ^ 1u);
             uint8_t* slot = ring1 + stage * kF1G1SlotBytes;
             mbar_arrive_expect_tx(&full1[stage], kF1StageBytes + kF1XChunkBytes);
             tma_load_2d_hint(slot, &tmW, &full1[stage], d0 + k * 64, row0, keep);
-            if (x_ready) {
-              tma_load_2d(slot + kF1StageBytes, &tmX, &full1[stage], d0 + k * 64, 0);
-            } else {
-              def_slot[ndef] = stage;
-              def_k[ndef] = k;
-              ++ndef;
-            }
+            if (x_ready) tma_load_2d(slot + kF1StageBytes, &tmX, &full1[stage], d0 + k * 64, 0);
+            else ++ndef;  // slot ndef (= stage), chunk k: X after the gather flags
             if (++stage == S1) {
               stage = 0;
               phase ^= 1u;
@@ -243,9 +243,10 @@ __global__ void __launch_bounds__(kF1Threads, 1)
           }
         }
         if (!x_ready) {  // fewer chunks than slots
-          wait_gathered();
+          for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
+          fence_proxy_async_global();
           for (int i = 0; i < ndef; ++i)
-            tma_load_2d(ring1 + def_slot[i] * kF1G1SlotBytes + kF1StageBytes, &tmX, &full1[def_slot[i]], d0 + def_k[i] * 64, 0);
+            tma_load_2d(ring1 + i * kF1G1SlotBytes + kF1StageBytes, &tmX, &full1[i], d0 + (i % KQ) * 64, 0);
         }
       } else if (!WHALE_SKIP(a.debug & 2)) {  // debug bit 2: timing experiment without G2
         for (int it = 0; it < my_tiles; ++it) {
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
           umma_bf16(tmem_base + ucol0 + i * kF1NB, ad, bd, idesc2, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&empty2[s2]);
+        if (j == my_tiles - 1) umma_commit(&ublk[i]);  // U block i is final: the epilogue writes it out
         if (++s2 == a.s2) {
           s2 = 0;
           ph2 ^= 1u;
@@ -622,14 +624,14 @@ __global__ void __launch_bounds__(kF1Threads, 1)
     }
     // ---- this CTA's part of U (relative to s_ref) -> global partials (lanes: consecutive d,
     //      128-byte warp stores; staging the 128 KB in smem for 1-D bulk copies measured slower)
+    //      Block m is written as soon as the last tile's G2 block m has completed (ublk[m]),
+    //      so the write-out overlaps the remaining G2 blocks of the last tile.
     const size_t ubase = static_cast<size_t>(cl) * a.Bt;
-    if (my_tiles > 0) {
-      mbar_wait(&pempty[(my_tiles - 1) & 1], ((my_tiles - 1) >> 1) & 1);
-      tc_fence_after();
-    }
     for (int m = 0; m < KQ / 2; ++m) {
       uint32_t u[16];
       if (my_tiles > 0) {
+        if (!WHALE_SKIP(a.debug & 2)) mbar_wait(&ublk[m], 0u);
+        tc_fence_after();
         tmem_ld16(tmem_base + ucol0 + m * kF1NB + c0 + lane_off, u);
         tmem_ld_wait();
       } else {

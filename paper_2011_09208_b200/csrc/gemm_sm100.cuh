@@ -154,9 +154,12 @@ __device__ __forceinline__ void decode_tile(const GemmArgs& a, int tile, int& mb
 
 // Hand an accumulator back to the MMA issuer: every epilogue thread arrives on tempty -- in a
 // CTA pair on the LEADER's barrier (its MMA overwrites both CTAs' halves).
+// Relaxed: the TMEM loads completed (tcgen05.wait::ld) before the fence, so the arrive orders
+// nothing else; .release would emit a GPU-scope MEMBAR per thread and tile (it waits for the
+// thread's outstanding global stores).
 __device__ __forceinline__ void release_acc(uint64_t* tempty_acc, bool pair) {
   tc_fence_before();
-  if (pair) mbar_arrive_remote_release(mapa_smem(smem_u32(tempty_acc), 0));
+  if (pair) mbar_arrive_remote(mapa_smem(smem_u32(tempty_acc), 0));
   else mbar_arrive(tempty_acc);
 }
 
@@ -522,21 +525,17 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
       // flags, then order the async-proxy (TMA) reads after them.  With the fused gather (K-major
       // A, no pairs) the first ring stages get their B loads at once and their A loads after
       // the wait (deferred), so W_r streams while the all-gather lands.
+      // (no lambdas / arrays: captured or indexed locals would live in local memory; the
+      // deferred stages are stages 0 .. ndef - 1, all in this CTA's first tile: k-blocks
+      // kb0f .. kb0f + ndef - 1 of M block mbf)
       bool a_ready = a.wait_flags == nullptr;
       const bool defer = !a_ready && a.gather_on && !PAIR && !A_MN;
-      auto wait_gathered = [&]() {
+      if (!a_ready && !defer) {
         for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
         fence_proxy_async_global();
         a_ready = true;
-      };
-      if (!a_ready && !defer) wait_gathered();
-      int ndef = 0;
-      int def_stage[8], def_kb[8], def_mb[8];
-      auto resolve = [&]() {  // gathered rows landed: the deferred A loads
-        wait_gathered();
-        for (int i = 0; i < ndef; ++i)
-          tma_load_2d(smem + def_stage[i] * a.stage_bytes, &tmA, &full[def_stage[i]], def_kb[i] * kBK, def_mb[i] * kBM);
-      };
+      }
+      int ndef = 0, kb0f = 0, mbf = 0;
       int stage = 0;
       uint32_t phase = 0;
       const int bk = (A_MN && B_MN) ? a.bk : kBK;
@@ -579,15 +578,22 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
             }
             continue;
           }
-          if (!a_ready && ndef == a.stages) resolve();  // (before waiting on a deferred stage)
+          if (!a_ready && (ndef == a.stages || tile != unit0)) {  // resolve before a deferred stage's reuse
+            for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
+            fence_proxy_async_global();
+            a_ready = true;
+            for (int i = 0; i < ndef; ++i)
+              tma_load_2d(smem + i * a.stage_bytes, &tmA, &full[i], (kb0f + i) * kBK, mbf * kBM);
+          }
           mbar_wait(&empty[stage], phase ^ 1u);
           mbar_arrive_expect_tx(&full[stage], tx);
           if (WHALE_SKIP(a.debug & 8)) {
             // timing experiment: A operand not loaded
           } else if (!a_ready) {
-            def_stage[ndef] = stage;  // A after the all-gather (K-major A only)
-            def_kb[ndef] = kb;
-            def_mb[ndef] = mb;
+            if (ndef == 0) {  // A after the all-gather (K-major A only)
+              kb0f = kb;
+              mbf = mb;
+            }
             ++ndef;
           } else if (!A_MN) {
             tma_load_2d(sA, &tmA, &full[stage], kb * kBK, mb * kBM);
@@ -608,7 +614,12 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
           }
         }
       }
-      if (!a_ready) resolve();  // fewer k-blocks than ring stages (or no tile)
+      if (!a_ready) {  // fewer k-blocks than ring stages (or no tile)
+        for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
+        fence_proxy_async_global();
+        for (int i = 0; i < ndef; ++i)
+          tma_load_2d(smem + i * a.stage_bytes, &tmA, &full[i], (kb0f + i) * kBK, mbf * kBM);
+      }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (pairs: the leader only, M = 256) =====================

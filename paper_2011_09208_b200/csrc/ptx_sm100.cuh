@@ -503,6 +503,18 @@ __device__ __forceinline__ void st_async_v4(uint32_t remote_addr, uint32_t remot
       "r"(a), "r"(b), "r"(c), "r"(d), "r"(remote_bar)
       : "memory");
 }
+// 4-byte asynchronous store into a peer CTA's smem; completes 4 bytes on the peer's mbarrier.
+__device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t remote_bar, uint32_t v) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote_addr), "r"(v),
+               "r"(remote_bar)
+               : "memory");
+}
+// Arrive on a peer CTA's mbarrier and raise its expected transaction bytes (relaxed: the bytes
+// themselves come with their own complete_tx, e.g. st.async).
+__device__ __forceinline__ void mbar_arrive_expect_tx_remote(uint32_t remote_bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(remote_bar), "r"(tx)
+               : "memory");
+}
 // Arrive on an mbarrier of a peer CTA.  Relaxed: used only to say "I have consumed the data
 // you wrote into my smem" after the values were loaded into registers (and a CTA barrier),
 // which needs no memory ordering; .release would emit a GPU-scope MEMBAR that waits for

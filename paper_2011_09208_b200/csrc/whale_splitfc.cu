@@ -374,6 +374,11 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
     // zero-padded half stage), which doubles the pipeline depth for the same smem.
     const int bk = (p.es == 2 && p.Bt <= 32) ? 32 : kbk;
     p.dw = choose_plain(p.Cr, p.D, p.Bt, atom, bk, sms);
+    const int force_bn = env_int("WHALE_DW_BN", 0);  // experiments: dW N tile (multiple of the atom)
+    if (force_bn >= atom && force_bn <= 256 && force_bn % atom == 0) {
+      p.dw.BN = force_bn;
+      p.dw.n_blocks = cdiv(p.D, force_bn);
+    }
     p.dw.bk = bk;
     finish_cfg(p.dw, sms, p.dw.num_kb <= 4, p.es, p.es == 2);
   }
@@ -427,7 +432,7 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   L.row_loss = take(p.Bt * 4);
   L.dxpart = take(static_cast<size_t>(p.dx.splits) * p.Bt * p.D * 4);
   L.counters = take(64 * 4);
-  L.tile_cnt = take(static_cast<size_t>(p.dx.m_blocks) * p.dx.n_blocks * 4);
+  L.tile_cnt = take(static_cast<size_t>(p.dx.m_blocks + 1) * p.dx.n_blocks * 4);  // +1: a CTA-pair padding block
   L.a_tile = take(static_cast<size_t>(p.Bt) * T * 4);
   L.dbpart = take(static_cast<size_t>(cdiv(p.Bt, kDbRows)) * p.Cr * 4);
   L.gscale = take(static_cast<size_t>(p.Bt) * T * 4);
@@ -563,6 +568,7 @@ struct whale_splitfc_ctx {
   bool gfuse = true;                 // G-fused backward (NEXT-4b): G formed from P~ in the bwd operand path
   bool row_bulk = false;             // dW tiles stored as 1-D bulk row copies (bwd_sm100.cuh)
   bool fused_gather = true;          // N > 1: bridge all-gather inside the logits / F1 prologue
+  bool bwd_pair = false;             // fused backward as CTA pairs (cta_group::2)
   bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
@@ -725,6 +731,8 @@ static whale_status_t preload_kernels() {
       reinterpret_cast<const void*>(splitfc_fwd_dx_kernel),
       reinterpret_cast<const void*>(splitfc_bwd_kernel<2, false>),
       reinterpret_cast<const void*>(splitfc_bwd_kernel<2, true>),
+      reinterpret_cast<const void*>(splitfc_bwd_kernel<2, false, true>),
+      reinterpret_cast<const void*>(splitfc_bwd_kernel<2, true, true>),
       reinterpret_cast<const void*>(stats_grad_kernel<2>),
       reinterpret_cast<const void*>(stats_grad_kernel<4>),
       reinterpret_cast<const void*>(stats_grad_multi_kernel<2>),
@@ -801,13 +809,30 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     return fail(WHALE_ERR_UNSUPPORTED, "bf16 dW needs the fused backward (WHALE_FUSED_BWD / WHALE_STORE_MODE overrides)");
   }
   if (c->fused_bwd) {
+    // CTA pairs in the fused backward (cta_group::2, M = 256 units over two M blocks): when dX
+    // needs no split-K (large B_tot x D: the tensor-bound shapes, e.g. c5) and both N tiles
+    // split into whole swizzle atoms per CTA.  Not with F1 (combine units) or the G-fused path.
+    const int atom = kRowBytes / p.es;
+    c->bwd_pair = !p.f1 && !c->gfuse && p.es == 2 && env_int("WHALE_BWD_PAIR", 1) != 0 && p.dx.splits == 1 &&
+                  p.dx.m_blocks >= 2 && p.dw.m_blocks >= 2 && p.dx.a_rows == kBM && (p.dx.BN / atom) % 2 == 0 &&
+                  (p.dw.BN / atom) % 2 == 0;
+    if (c->bwd_pair) {
+      for (GemmCfg* g : {&c->p.dx, &c->p.dw}) {
+        g->cluster = 2;
+        g->m_blocks += g->m_blocks & 1;  // an odd M block count gets one all-padding tile
+        g->num_tiles = g->m_blocks * g->n_blocks * g->splits;
+      }
+      const int kbk = kRowBytes / p.es;
+      c->p.dx.stage_bytes = kBM * kRowBytes + (p.dx.BN / 2 / atom) * kbk * kRowBytes;  // own A + half of B
+      c->p.dw.stage_bytes = (kBM / atom) * p.dw.bk * kRowBytes + (p.dw.BN / 2 / atom) * p.dw.bk * kRowBytes;
+    }
     // F1: the backward runs dW tiles only (dX came from the forward)
     c->bwd_stage_bytes = p.f1 ? p.dw.stage_bytes : std::max(p.dx.stage_bytes, p.dw.stage_bytes);
     // CTA-wide 16 KB store stages: dW-only (F1) deep; with dX units the load ring wants the
     // smem (measured: 2 store stages + 4 load stages beat 4 + 3 at c4 / c5 by 7-11 %)
-    c->bwd_epi_bufs = env_int("WHALE_BWD_EPI", p.f1 ? 8 : 2);
+    c->bwd_epi_bufs = env_int("WHALE_BWD_EPI", p.f1 ? 8 : (c->bwd_pair ? 4 : 2));
     // dW-only schedule (F1): row-bulk dW stores need 128 padded rows of BN fp32 of staging
-    c->row_bulk = p.f1 && env_int("WHALE_ROW_BULK", 1) != 0;
+    c->row_bulk = (p.f1 && env_int("WHALE_ROW_BULK", 1) != 0) || env_int("WHALE_ROW_BULK", 1) == 2;
     if (c->row_bulk)
       c->bwd_epi_bufs = std::max(c->bwd_epi_bufs, (kBM * (p.dw.BN + 4) * 4 + 4 * kEpiBufBytes - 1) / (4 * kEpiBufBytes));
     const int fixed = 1024 + 512 + c->bwd_epi_bufs * 4 * kEpiBufBytes;
@@ -1303,15 +1328,45 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     b.stage_bytes = c->bwd_stage_bytes;
     b.epi_bufs = c->bwd_epi_bufs;
     b.sched_cnt = counters + CNT_SCHED;
-    const int grid = std::min(b.ux + b.tw + b.tc, p.sms);
-    auto kern = p.dw_bf16 ? splitfc_bwd_kernel<2, true> : splitfc_bwd_kernel<2, false>;
-    {
-      const whale_status_t st = ensure_smem_attr(kern, p.dw_bf16 ? 9 : 8);
-      if (st != WHALE_OK) return st;
+    if (c->bwd_pair) {  // CTA pairs: units are pair tiles, the grid is 2-CTA clusters
+      b.ux = p.dx.num_tiles / 2;
+      b.tw = p.dw.num_tiles / 2;
+      const int grid = 2 * std::min(b.ux + b.tw, p.sms / 2);
+      auto kern = p.dw_bf16 ? splitfc_bwd_kernel<2, true, true> : splitfc_bwd_kernel<2, false, true>;
+      {
+        const whale_status_t st = ensure_smem_attr(kern, p.dw_bf16 ? 19 : 18);
+        if (st != WHALE_OK) return st;
+      }
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kBwdThreads);
+      cfg.dynamicSmemBytes = c->bwd_smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = c->pdl ? 2 : 1;
+      PROFILED(K_BWD, s, ([&]() -> whale_status_t {
+                 CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, c->tmG_dx, c->tmW_dx, c->tmDxPart, c->tmG_dw, c->tmX_dw,
+                                             c->tmDW, b));
+                 return WHALE_OK;
+               }()));
+    } else {
+      const int grid = std::min(b.ux + b.tw + b.tc, p.sms);
+      auto kern = p.dw_bf16 ? splitfc_bwd_kernel<2, true> : splitfc_bwd_kernel<2, false>;
+      {
+        const whale_status_t st = ensure_smem_attr(kern, p.dw_bf16 ? 9 : 8);
+        if (st != WHALE_OK) return st;
+      }
+      PROFILED(K_BWD, s,
+               (launch(c, kern, dim3(grid), dim3(kBwdThreads), c->bwd_smem, s, c->tmG_dx, c->tmW_dx, c->tmDxPart,
+                       c->tmG_dw, c->tmX_dw, c->tmDW, b)));
     }
-    PROFILED(K_BWD, s,
-             (launch(c, kern, dim3(grid), dim3(kBwdThreads), c->bwd_smem, s, c->tmG_dx, c->tmW_dx, c->tmDxPart,
-                     c->tmG_dw, c->tmX_dw, c->tmDW, b)));
   } else if constexpr (ES == 2) {
     // ---- A7 dW_r = G_r^T X  (A = G^T MN-major, B = X MN-major); on the F1 path dX came from
     //      the combine kernel above, so this launch ends the step
@@ -1485,6 +1540,11 @@ extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, cha
                   ",\"off_dxpart\":" + std::to_string(p.L.dxpart) + ",\"f1\":" + std::to_string(p.f1 ? 1 : 0) +
                   ",\"f1_clusters\":" + std::to_string(p.f1_ncl) + ",\"f1_stages\":" + std::to_string(p.f1_stages) +
                   ",\"nvls\":" + std::to_string(ctx->mc != nullptr ? 1 : 0) +
+                  ",\"fused_bwd\":" + std::to_string(ctx->fused_bwd ? 1 : 0) +
+                  ",\"bwd_pair\":" + std::to_string(ctx->bwd_pair ? 1 : 0) +
+                  ",\"bwd_stages\":" + std::to_string(ctx->bwd_stages) +
+                  ",\"bwd_epi_bufs\":" + std::to_string(ctx->bwd_epi_bufs) +
+                  ",\"fused_gather\":" + std::to_string(ctx->fused_gather ? 1 : 0) +
                   ",\"local_bytes\":" + std::to_string(p.L.local_total) +
                   ",\"symm_bytes\":" + std::to_string(p.L.symm_total) + "}";
   if (s.size() + 1 > buf_len) return fail(WHALE_ERR_INVALID_ARG, "buffer too small (%zu)", s.size() + 1);

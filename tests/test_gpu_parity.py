@@ -470,6 +470,49 @@ def test_cta_pair_mma(whale, B, D, C, fused, monkeypatch):
     op.close()
 
 
+@pytest.mark.parametrize("B,D,C", [(1024, 4096, 3001), (1152, 4096, 1003)])
+def test_bwd_cta_pairs(whale, B, D, C, monkeypatch):
+    """CTA pairs in the fused backward (cta_group::2, M = 256 units; the leader's scheduler hands
+    each unit to the peer through DSMEM): on by default when dX needs no split-K (here 8 x 16 and
+    9 x 16 tiles -- the odd M-block count gets a padding tile).  Against the oracle (fp32 dW),
+    against the unpaired kernel, and bf16 dW = the fp32 dW rounded once."""
+    seed = 700 + B
+    X = syn.gen_features((0, B), D, seed, "bf16")
+    W = syn.gen_weight((0, C), D, seed, "peaked", "bf16")
+    y = syn.gen_labels((0, B), C, seed)
+    op = whale.SplitFCSoftmaxCE(C, D, B)
+    cfg = op.config()
+    assert cfg["bwd_pair"] == 1 and cfg["dx"]["cluster"] == 2, cfg
+    xd, wd, yd = X.cuda(), W.cuda(), y.cuda()
+    loss = float(op.forward(xd, yd, wd, row_loss=True))
+    dx, dw = [t.clone() for t in op.backward(wd)]
+    op.check()
+    f = oracle.forward_backward(X, W, y.numpy())
+    assert abs(loss - f["loss"]) <= LOSS_RTOL * f["loss"]
+    assert _fro(dx.float().cpu(), f["dX"]) <= FRO_RTOL
+    assert _fro(dw.cpu(), f["dW"]) <= FRO_RTOL
+    for k, g in (("dX", dx.float().cpu().numpy()), ("dW", dw.cpu().numpy())):
+        scale = np.abs(f[k]).max()
+        assert np.abs(g - f[k]).max() <= 2e-2 * scale, k
+    op.close()
+    monkeypatch.setenv("WHALE_BWD_PAIR", "0")
+    op0 = whale.SplitFCSoftmaxCE(C, D, B)
+    assert op0.config()["bwd_pair"] == 0
+    op0.forward(xd, yd, wd)
+    dx0, dw0 = op0.backward(wd)
+    op0.check()
+    assert _fro(dw.cpu(), dw0.cpu()) <= 1e-5 and _fro(dx.float().cpu(), dx0.float().cpu()) <= 1e-2
+    op0.close()
+    monkeypatch.delenv("WHALE_BWD_PAIR")
+    opb = whale.SplitFCSoftmaxCE(C, D, B, dw_dtype=torch.bfloat16)
+    assert opb.config()["bwd_pair"] == 1
+    opb.forward(xd, yd, wd)
+    _, dwb = opb.backward(wd)
+    opb.check()
+    assert torch.equal(dwb, dw.to(torch.bfloat16))
+    opb.close()
+
+
 @pytest.mark.parametrize("B,D,C", [(32, 1024, 9001), (200, 520, 3001), (300, 1024, 20_000)])
 def test_gfused_backward_matches_materialised(whale, B, D, C, monkeypatch):
     """NEXT-4b: the G-fused backward (G formed from P~ in the operand path) computes the same
