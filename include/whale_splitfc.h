@@ -137,8 +137,11 @@ typedef struct whale_splitfc_desc {
    * multimem store then reaches the same offset in every rank's buffer through the NVSwitch.
    * Used for the bridge all-gather (A2) of X_r, y_r and its flags (the B200
    * form of the all-gather the paper's bridge inserts); NULL keeps the
-   * unicast peer stores.  The reduce-scatter stays unicast (its fixed summation order keeps
-   * dX bitwise reproducible; a switch reduction would not). */
+   * unicast peer stores.  With WHALE_NVLS_RS=1 the dX reduce-scatter (A8) goes through the
+   * switch as well: every rank stores its rows for owner q in slot q of its OWN receive slab
+   * and the owner reads all ranks' slot at once with multimem.ld_reduce (parity-green and
+   * run-to-run reproducible at N = 2; off by default: measured slower than the unicast
+   * pushes + rank-ordered sum, which stays the default). */
   void* multicast_ptr;
 } whale_splitfc_desc;
 

@@ -408,11 +408,13 @@ __global__ void __launch_bounds__(kStatsThreads) stats_grad_multi_kernel(const S
 // ---------------------------------------------------------------- A8 dX reduce-scatter (owner)
 // The dX GEMM's fixup pushed every peer's reduced rows into recv[p][B_r x D] (slabs of
 // B_max rows) and raised flag[RS][p]; wait for all, then dX_r = sum_p recv[p] in rank order.
+// NVLS (mc_mine != NULL): every rank left its rows for this owner in slot `rank` of its OWN
+// slab; one multimem.ld_reduce per 16 bytes returns their sum, formed in the NVSwitch.
 template <int ES>
 __global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict__ recv, int B, int B_slab, int D,
                                                         int world,
                                                         const uint32_t* my_flags, const uint32_t* dev_epoch,
-                                                        void* dx_local, int* err) {
+                                                        void* dx_local, int* err, const float4* mc_mine) {
   pdl_wait();
   pdl_trigger();
   TraceScope _trace(6);
@@ -425,10 +427,15 @@ __global__ void __launch_bounds__(256) dx_reduce_kernel(const float4* __restrict
   const int64_t slab = static_cast<int64_t>(B_slab) * (D / 4);
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float4 acc = __ldcg(recv + e);
-    for (int p = 1; p < world; ++p) {
-      const float4 v = __ldcg(recv + p * slab + e);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    float4 acc;
+    if (mc_mine != nullptr) {
+      acc = multimem_ld_reduce_add_v4f32(mc_mine + e);
+    } else {
+      acc = __ldcg(recv + e);
+      for (int p = 1; p < world; ++p) {
+        const float4 v = __ldcg(recv + p * slab + e);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
     }
     if constexpr (ES == 2) {
       __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);

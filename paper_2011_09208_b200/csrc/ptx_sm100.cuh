@@ -380,6 +380,15 @@ __device__ __forceinline__ void multimem_st_u32(void* mc, uint32_t v) {
 __device__ __forceinline__ void multimem_red_add_release_u32(void* mc, uint32_t v) {
   asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
 }
+// Load of the same 16 bytes from every rank's buffer, summed in the NVSwitch.
+__device__ __forceinline__ float4 multimem_ld_reduce_add_v4f32(const void* mc) {
+  float4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(mc)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ void multimem_red_add_relaxed_u32(void* mc, uint32_t v) {
   asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
 }

@@ -569,6 +569,7 @@ struct whale_splitfc_ctx {
   bool row_bulk = false;             // dW tiles stored as 1-D bulk row copies (bwd_sm100.cuh)
   bool fused_gather = true;          // N > 1: bridge all-gather inside the logits / F1 prologue
   bool bwd_pair = false;             // fused backward as CTA pairs (cta_group::2)
+  bool nvls_rs = false;              // dX reduce-scatter through the NVSwitch (multimem.ld_reduce)
   bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
@@ -785,6 +786,9 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     }
     for (int r = 0; r < p.world; ++r) c->symm[r] = static_cast<uint8_t*>(desc->peer_symm_ptrs[r]);
     c->mc = static_cast<uint8_t*>(desc->multicast_ptr);
+    // NVLS reduce-scatter (multimem.ld_reduce): parity-green and bitwise reproducible at N = 2,
+    // but measured slower than the unicast pushes (owner reduce 12.8 -> 17.0 us): opt-in
+    c->nvls_rs = c->mc != nullptr && env_int("WHALE_NVLS_RS", 0) != 0;
   }
   const char* pdl_env = getenv("WHALE_PDL");
   // WHALE_SHARED_DEVICE=1: several ranks share this device (the single-GPU multi-rank test
@@ -1188,6 +1192,19 @@ extern "C" whale_status_t whale_splitfc_forward_ex(whale_splitfc_ctx* ctx, const
   return st;
 }
 
+
+// Destination of the dX rows this rank sends to owner q (A8 reduce-scatter).  Unicast: slot
+// `rank` of q's receive slab (an NVLink store).  NVLS (multicast mapping present): slot q of
+// THIS rank's own slab (a local store) -- the owner later reads slot q of every rank summed in
+// the NVSwitch (multimem.ld_reduce).  Expressed as the base the kernels index with
+// [rank * B_slab + row] * D, so the push code is the same for both.
+static uint8_t* rs_dst_base(const whale_splitfc_ctx* c, int q) {
+  const Plan& p = c->p;
+  if (!c->nvls_rs) return c->symm[q] + p.L.dxrecv;
+  const int64_t slab = static_cast<int64_t>(p.Bmax) * p.D * 4;
+  return c->symm[p.rank] + p.L.dxrecv + (static_cast<int64_t>(q) - p.rank) * slab;
+}
+
 // ============================================================================ backward
 template <int ES>
 static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* dx_local, void* dw, float* db,
@@ -1251,7 +1268,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
   } else {
     ax.fix_mode = FIX_PUSH;
     for (int r = 0; r < p.world; ++r) {
-      ax.recv.p[r] = c->symm[r] + L.dxrecv;
+      ax.recv.p[r] = rs_dst_base(c, r);
       ax.rs_flags.p[r] = reinterpret_cast<uint32_t*>(c->symm[r] + L.flags) + FLAG_RS * kMaxRanks + p.rank;
     }
   }
@@ -1262,7 +1279,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     PeerPtrs recv{};
     for (int r = 0; r <= p.world; ++r) rs.off[r] = static_cast<int>(p.Boff[r]);
     if (p.world > 1)
-      for (int r = 0; r < p.world; ++r) recv.p[r] = c->symm[r] + L.dxrecv;
+      for (int r = 0; r < p.world; ++r) recv.p[r] = rs_dst_base(c, r);
     PROFILED(K_DX, s,
              (launch(c, dx_combine_kernel<2>, dim3(cdiv(p.D / 4, 32), static_cast<unsigned>(p.Bt)), dim3(256), 0,
                      s, static_cast<const float*>(wsp<float>(c, L.upart)),
@@ -1302,7 +1319,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       cb.dx_out = dx_local;
       for (int r = 0; r <= p.world; ++r) cb.row_off[r] = static_cast<int>(p.Boff[r]);
       if (p.world > 1)
-        for (int r = 0; r < p.world; ++r) cb.recv.p[r] = c->symm[r] + L.dxrecv;
+        for (int r = 0; r < p.world; ++r) cb.recv.p[r] = rs_dst_base(c, r);
       cb.rank = p.rank;
       cb.world = p.world;
       cb.Bslab = static_cast<int>(p.Bmax);
@@ -1418,11 +1435,15 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     const int g2 = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(cdiv(own, 256), c->shared_device ? std::max(1, p.sms / 8) : 2 * p.sms)));
     const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_RS * kMaxRanks;
+    // NVLS: slot `rank` of every rank's slab, summed in the switch (multicast view)
+    const float4* mc_mine =
+        c->nvls_rs ? reinterpret_cast<const float4*>(c->mc + L.dxrecv + static_cast<size_t>(p.rank) * p.Bmax * p.D * 4)
+                   : nullptr;
     PROFILED(K_RS_REDUCE, s,
              (launch(c, dx_reduce_kernel<ES>, dim3(g2), dim3(256), 0, s,
                      reinterpret_cast<const float4*>(c->symm[p.rank] + L.dxrecv), static_cast<int>(p.B),
                      static_cast<int>(p.Bmax), static_cast<int>(p.D), p.world, my_flags, static_cast<const uint32_t*>(dev_epoch), dx_local,
-                     err)));
+                     err, mc_mine)));
   }
   return WHALE_OK;
 }
@@ -1540,6 +1561,7 @@ extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, cha
                   ",\"off_dxpart\":" + std::to_string(p.L.dxpart) + ",\"f1\":" + std::to_string(p.f1 ? 1 : 0) +
                   ",\"f1_clusters\":" + std::to_string(p.f1_ncl) + ",\"f1_stages\":" + std::to_string(p.f1_stages) +
                   ",\"nvls\":" + std::to_string(ctx->mc != nullptr ? 1 : 0) +
+                  ",\"nvls_rs\":" + std::to_string(ctx->nvls_rs ? 1 : 0) +
                   ",\"fused_bwd\":" + std::to_string(ctx->fused_bwd ? 1 : 0) +
                   ",\"bwd_pair\":" + std::to_string(ctx->bwd_pair ? 1 : 0) +
                   ",\"bwd_stages\":" + std::to_string(ctx->bwd_stages) +

@@ -78,6 +78,15 @@ def run_case(rank, world, dev, B, D, C, capacity=None, regime="init", dtype="bf1
             res["prob_rel"] = float(np.max(np.abs(op.prob.cpu().numpy() - f["prob"][rows]) / f["prob"][rows])) if B else 0.0
             ok_s = ok_s and res["db_rel"] <= 1e-2 and res["pred_ok"] and res["prob_rel"] <= 1e-3
         ok = ok and ok_s
+    # run-to-run reproducibility of the reduce-scattered dX and of dW: the last step again
+    dx_last, dw_last = dx.clone(), dw.clone()
+    op.forward(xr, yr, wr, bias=br, predictions=bias)
+    out = op.backward(wr, bias_grad=bias)
+    op.check()
+    res["dx_repeat_bitwise"] = bool(torch.equal(out[0], dx_last))
+    res["dw_repeat_bitwise"] = bool(torch.equal(out[1], dw_last))
+    res["nvls_rs"] = op.config().get("nvls_rs", 0)
+    ok = ok and res["dx_repeat_bitwise"] and res["dw_repeat_bitwise"]
     res["ok"] = ok
     allres = [None] * world
     dist.all_gather_object(allres, res)
