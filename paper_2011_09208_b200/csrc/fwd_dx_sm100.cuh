@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(kF1Threads, 1)
           for (int j = 0; j < my_tiles; ++j) {
             mbar_wait(&pfull[j & 1], static_cast<uint32_t>((j >> 1) & 1));  // P~_j^T in smem, U rescaled
             tc_fence_after();
+            if (WHALE_SKIP(a.debug & 2)) {  // timing experiment without G2: keep the P~ protocol alive
+              mbar_arrive(&pempty[j & 1]);
+              continue;
+            }
             for (int i = 0; i < KQ / 2; ++i) g2_block(j, i);
             umma_commit(&pempty[j & 1]);
             if (dbg && j < 64) g_f1_ts[j * 16 + 2] = gtime_ns();
@@ -648,7 +652,7 @@ __global__ void __launch_bounds__(kF1Threads, 1)
     if (a.debug & 32) __threadfence();  // timing experiment: drain the stores before the end stamp
     // the peers' last remote operation on this CTA's shared memory is their "consumed"
     // arrive for the last tile's partial: once it has landed nothing targets this CTA
-    if (my_tiles > 0) mbar_wait(xempty, (my_tiles - 1) & 1);
+    if (my_tiles > 0 && !WHALE_SKIP(a.debug & 4)) mbar_wait(xempty, (my_tiles - 1) & 1);
   }
   // debug timeline: the exit stamps are kept in registers and stored together at the end (a
   // store between two timer reads would time its own issue stall)
