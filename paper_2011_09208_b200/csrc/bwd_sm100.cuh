@@ -175,6 +175,9 @@ __device__ __forceinline__ void combine_unit(const CombineArgs& c, int u, float*
 }
 
 constexpr int kSchedSlots = 4;
+// Debug timeline (WHALE_EPI_DEBUG bit 16, no effect on results): per CTA [start, dX unit done
+// (after its fixup), epilogue done, GEMM units] in globaltimer ns -- whale_debug_bwd_timeline.
+__device__ unsigned long long g_bwd_cta[160 * 4];
 
 // DWB: dW_r stored in bf16 (a separate instantiation, so the fp32 kernel carries none of the
 // bf16 store code and keeps its register allocation)
@@ -269,6 +272,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     else mbar_arrive(bar);
   };
   const uint32_t e = ld_acquire_gpu(a.dx.dev_epoch) + 1u;  // this step's epoch
+  if ((a.dx.debug & 16) && threadIdx.x == 0 && blockIdx.x < 160) {
+    g_bwd_cta[blockIdx.x * 4] = gtime_ns();
+    g_bwd_cta[blockIdx.x * 4 + 1] = 0ull;
+  }
 
   if (warp == 0) {
     // ===================== scheduler + TMA producer =====================
@@ -575,9 +582,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         named_bar_sync(1, 128);
         __threadfence();
         fixup_share<ES>(a.dx, mb, nb, sp, threadIdx.x - 128);
+        if ((a.dx.debug & 16) && threadIdx.x == 128 && blockIdx.x < 160) g_bwd_cta[blockIdx.x * 4 + 1] = gtime_ns();
       }
     }
     if (threadIdx.x == 128 || a.row_bulk) bulk_wait<0>();  // this thread's bulk stores are complete
+    if ((a.dx.debug & 16) && threadIdx.x == 128 && blockIdx.x < 160) {
+      g_bwd_cta[blockIdx.x * 4 + 2] = gtime_ns();
+      g_bwd_cta[blockIdx.x * 4 + 3] = static_cast<unsigned long long>(na);
+    }
   } else if (warp >= 8 && xf) {
     // ===================== G-fused operand transformers =====================
     // thread tt owns one 128-byte row of every A stage.  The stages are walked as a task

@@ -255,14 +255,19 @@ __device__ __forceinline__ void fixup_share(const GemmArgs& a, int mb, int nb, i
 // between are harmless -- and publishes the step epoch for the following kernels.
 __device__ __forceinline__ void end_of_step_ticket(const GemmArgs& a, uint32_t e, int& s_last,
                                                    unsigned* sched_cnt = nullptr) {
+  // the RS flags (N > 1) publish this rank's dX pushes to the peers: system scope; at N = 1
+  // the ticket orders only this GPU's kernels (gpu scope)
+  const bool sys = a.rs_signal != 0 || (a.debug & 32);  // (debug bit 32: the old sys fences, for A/B)
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    if (sys) __threadfence_system();
+    else __threadfence();
     const uint32_t done = atomicAdd(a.done_cnt, 1u) + 1u;
     s_last = (done == gridDim.x);
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence_system();
+  if (sys) __threadfence_system();
+  else __threadfence();
   if (threadIdx.x < a.world && a.rs_signal) st_relaxed_sys(a.rs_flags.p[threadIdx.x], e);  // fenced above
   if (a.tile_cnt != nullptr)
     for (int k = threadIdx.x; k < a.m_blocks * a.n_blocks; k += blockDim.x) a.tile_cnt[k] = 0u;

@@ -1625,6 +1625,13 @@ extern "C" int whale_debug_f1_max_clusters(int smem) {
   return n;
 }
 
+// Internal: read the backward debug timeline (160 CTAs x {start, dX unit done, epilogue done,
+// GEMM units}; WHALE_EPI_DEBUG=16).  Synchronises the device.
+extern "C" int whale_debug_bwd_timeline(unsigned long long* out) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  return cudaMemcpyFromSymbol(out, g_bwd_cta, sizeof(g_bwd_cta)) == cudaSuccess ? 0 : -2;
+}
+
 // Internal: read the F1 debug timeline (64 periods x 16 stamps, then 160 CTAs x {entry, start, end,
 // after cluster sync, exit}, ns).  Synchronises the device.
 extern "C" int whale_debug_f1_timeline(unsigned long long* out) {

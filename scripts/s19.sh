@@ -1,0 +1,14 @@
+set -u
+O=gpurun_out/s19; mkdir -p $O
+N=$(nvidia-smi -L | wc -l)
+timeout 900 python -m torch.distributed.run --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29671 tests/mgpu_parity_worker.py > $O/mg.log 2>&1; echo "worker rc=$?"
+python - <<PY
+import json
+rs=[json.loads(l) for l in open("$O/mg.log") if l.startswith("{")]
+print(len(rs), "results; all ok:", all(r["ok"] for r in rs), "nvls:", {r.get("nvls") for r in rs}, "dx_rep:", all(r.get("dx_repeat_bitwise") for r in rs), "max dx_rel", max(r["dx_rel"] for r in rs), "max dw_rel", max(r["dw_rel"] for r in rs))
+PY
+for CF in c2 c3; do
+timeout 300 python -m torch.distributed.run --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29672 bench.py --gpus $N --config $CF --steps 30 --warmup 5 > $O/b_$CF.json 2> $O/b_$CF.err; echo "bench $CF rc=$?"
+python -c "import json;d=json.loads(open('$O/b_$CF.json').read().strip().splitlines()[-1]);print('$CF N=$N', round(d['ms_per_step']*1e3,1), round(d['value']), {k:round(v['avg_us'],1) for k,v in d['kernels'].items()}, d['clocks'])"
+done
+CFG=c2 timeout 300 python -m torch.distributed.run --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29673 scripts/trace_step.py > $O/trace.txt 2>&1; grep '"it": 4' $O/trace.txt

@@ -75,6 +75,19 @@ if os.environ.get("WHALE_F1_DBG"):  # F1 per-CTA [entry, after prologue, end] of
         if os.environ.get("F1_CTA_DUMP"):
             rel = lambda v: [round((x - t0) / 1e3, 2) for x in v]
             json.dump({"entry": rel(ent), "end": rel(en), "sync": rel(cs), "exit": rel(ex)}, open(os.environ["F1_CTA_DUMP"], "w"))
+if os.environ.get("BWD_TL"):  # backward per-CTA timeline (needs WHALE_EPI_DEBUG=16)
+    L.whale_debug_bwd_timeline.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+    tb = (ctypes.c_ulonglong * 640)()
+    L.whale_debug_bwd_timeline(tb)
+    n = sum(1 for c in range(160) if tb[4 * c])
+    st = [tb[4 * c] for c in range(n)]
+    dxd = [tb[4 * c + 1] for c in range(n) if tb[4 * c + 1]]
+    en = [tb[4 * c + 2] for c in range(n)]
+    units = [tb[4 * c + 3] for c in range(n)]
+    b0 = min(st)
+    q = lambda v: [round((x - b0) / 1e3, 1) for x in (min(v), sorted(v)[len(v) // 2], max(v))] if v else []
+    print(json.dumps({"rank": rank, "bwd_ctas": n, "start_min_med_max": q(st), "dx_done": q(dxd),
+                      "end": q(en), "units_min_max": [min(units), max(units)]}))
 op.check()
 if group is not None:
     allo = [None] * world
