@@ -172,6 +172,9 @@ __device__ __forceinline__ void combine_unit(const CombineArgs& c, int u, float*
     }
   }
   named_bar_sync(1, 128);  // fac is reused by the next unit
+  // N > 1: the pushes of this unit, published at system scope now (the end-of-step ticket
+  // then needs only gpu-scope fences in every CTA but the last)
+  if (c.world > 1 && threadIdx.x == 128) __threadfence_system();
 }
 
 constexpr int kSchedSlots = 4;
@@ -582,6 +585,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         named_bar_sync(1, 128);
         __threadfence();
         fixup_share<ES>(a.dx, mb, nb, sp, threadIdx.x - 128);
+        if (a.dx.fix_mode == FIX_PUSH) {  // this CTA's NVLink pushes, published at system scope now
+          named_bar_sync(1, 128);         // (off the kernel's tail: the dW tiles follow)
+          if (threadIdx.x == 128) __threadfence_system();
+        }
         if ((a.dx.debug & 16) && threadIdx.x == 128 && blockIdx.x < 160) g_bwd_cta[blockIdx.x * 4 + 1] = gtime_ns();
       }
     }
@@ -701,7 +708,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if constexpr (PAIR) tmem_dealloc_pair(tmem_base, kTmemCols);
     else tmem_dealloc(tmem_base, kTmemCols);
   }
-  end_of_step_ticket(a.dx, e, s_fix_go, a.sched_cnt);  // RS flags (N > 1) + epoch publish + counter reset
+  end_of_step_ticket(a.dx, e, s_fix_go, a.sched_cnt, /*pushes_fenced=*/true);  // RS flags (N > 1) + epoch publish + counter reset
 }
 
 }  // namespace whale

@@ -253,13 +253,15 @@ __device__ __forceinline__ void fixup_share(const GemmArgs& a, int mb, int nb, i
 // re-arms the launch-local counters (done ticket, split-K tile counters, the dynamic
 // scheduler) for the next backward -- they depend on no epoch, so forward-only steps in
 // between are harmless -- and publishes the step epoch for the following kernels.
+// pushes_fenced: every CTA already published its NVLink pushes with a system-scope fence right
+// after them (the fused backward), so only the last CTA, which raises the RS flags, needs one.
 __device__ __forceinline__ void end_of_step_ticket(const GemmArgs& a, uint32_t e, int& s_last,
-                                                   unsigned* sched_cnt = nullptr) {
+                                                   unsigned* sched_cnt = nullptr, bool pushes_fenced = false) {
   // the RS flags (N > 1) publish this rank's dX pushes to the peers: system scope; at N = 1
   // the ticket orders only this GPU's kernels (gpu scope)
   const bool sys = a.rs_signal != 0 || (a.debug & 32);  // (debug bit 32: the old sys fences, for A/B)
   if (threadIdx.x == 0) {
-    if (sys) __threadfence_system();
+    if (sys && !pushes_fenced) __threadfence_system();
     else __threadfence();
     const uint32_t done = atomicAdd(a.done_cnt, 1u) + 1u;
     s_last = (done == gridDim.x);
