@@ -564,6 +564,8 @@ struct whale_splitfc_ctx {
   uint32_t bwd_epoch = 0;            // backward count (fixup counters)
   bool have_fwd = false;
   bool pdl = false;
+  int pdl_mask = 0;                  // per-kernel PDL (WHALE_PDL_MASK): 1 stats, 2 backward, 4 owner reduce, 8 logits/F1
+  int cur_kbit = 0;                  // the PDL bit of the launch being issued
   bool fused_bwd = true;             // dW + dX in one persistent launch (bf16)
   bool gfuse = true;                 // G-fused backward (NEXT-4b): G formed from P~ in the bwd operand path
   bool row_bulk = false;             // dW tiles stored as 1-D bulk row copies (bwd_sm100.cuh)
@@ -583,6 +585,14 @@ static T* wsp(whale_splitfc_ctx* c, size_t off) {
   return reinterpret_cast<T*>(c->ws + off);
 }
 
+// PDL for the launch being issued (WHALE_PDL=1: every launch; WHALE_PDL_MASK: selected
+// kernels); consumes the launch's PDL bit.
+static bool pdl_for(whale_splitfc_ctx* c) {
+  const bool on = c->pdl || (c->pdl_mask & c->cur_kbit) != 0;
+  c->cur_kbit = 0;
+  return on;
+}
+
 // Launch with programmatic dependent launch (PDL): kernels call griddepcontrol.wait.
 template <typename... KArgs, typename... Args>
 static whale_status_t launch(whale_splitfc_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -596,7 +606,7 @@ static whale_status_t launch(whale_splitfc_ctx* c, void (*kern)(KArgs...), dim3 
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = c->pdl ? 1 : 0;
+  cfg.numAttrs = pdl_for(c) ? 1 : 0;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
   return WHALE_OK;
 }
@@ -645,7 +655,7 @@ static whale_status_t launch_gemm(whale_splitfc_ctx* c, int slot, const GemmCfg&
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = c->pdl ? 2 : 1;
+  cfg.numAttrs = pdl_for(c) ? 2 : 1;
   CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, A, B, O, args));
   return WHALE_OK;
 }
@@ -800,6 +810,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   // (c2 N=1 249.0 -> 248.1 us, N=2 194 -> 189, c4 1265 -> 1176, c5 10.65 -> 10.38 ms without
   // it); WHALE_PDL=1 turns it on (the kernels' griddepcontrol.wait keeps either mode correct)
   c->pdl = (pdl_env && pdl_env[0] == '1') && !c->shared_device;
+  c->pdl_mask = c->shared_device ? 0 : env_int("WHALE_PDL_MASK", 0);
   {
     // peer-wait timeout (flags, LL records, split-K counters): WHALE_TIMEOUT_MS, default 300 s
     const unsigned long long ns = static_cast<unsigned long long>(std::max(1, env_int("WHALE_TIMEOUT_MS", 300000))) * 1000000ull;
@@ -1063,7 +1074,8 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = c->pdl ? 2 : 1;
+    c->cur_kbit = 8;  // PDL bit of the logits / F1 launch
+    cfg.numAttrs = pdl_for(c) ? 2 : 1;
     PROFILED(K_LOGITS, s, ([&]() -> whale_status_t {
                CUDA_TRY(cudaLaunchKernelEx(&cfg, splitfc_fwd_dx_kernel, c->tmW_f1, c->tmX_f1, c->tmP_f1, a));
                return WHALE_OK;
@@ -1086,6 +1098,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
       a.gather_on = gather_fused ? 1 : 0;
       a.gather = gth;
     }
+    c->cur_kbit = 8;
     PROFILED(K_LOGITS, s,
              (launch_gemm<EPI_FWD_STATS, false, false, ES>(c, ES == 2 ? 0 : 3, p.fwd, c->tmX_fwd,
                                                            c->tmW_fwd, c->tmP_store, a, s)));
@@ -1144,7 +1157,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     if (p.world == 1) {
       // A4-A6 fused: lse, loss and G (or its factors) in one pass (no exchange needed)
       PROFILED(K_STATS, s,
-               (launch(c, stats_grad_kernel<ES>, dim3(gy, p.Bt), dim3(kStatsThreads), 0, s, a, P,
+               (c->cur_kbit = 1, launch(c, stats_grad_kernel<ES>, dim3(gy, p.Bt), dim3(kStatsThreads), 0, s, a, P,
                        static_cast<long long>(p.ldp), p.fwd.BN, inv_bt)));
     } else {
       // A4-A6 fused with the per-row cross-GPU exchange (chunk-0 CTAs of every row first)
@@ -1153,7 +1166,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
       const int gx = c->shared_device ? std::max(1, std::min(static_cast<int>(p.Bt), p.sms / 8)) : static_cast<int>(p.Bt);
       if (c->shared_device) gy = std::min(gy, 2);
       PROFILED(K_STATS, s,
-               (launch(c, stats_grad_multi_kernel<ES>, dim3(gx, gy), dim3(kStatsThreads), 0, s, a, P,
+               (c->cur_kbit = 1, launch(c, stats_grad_multi_kernel<ES>, dim3(gx, gy), dim3(kStatsThreads), 0, s, a, P,
                        static_cast<long long>(p.ldp), p.fwd.BN, inv_bt)));
     }
   }
@@ -1367,7 +1380,8 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
       at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[1].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at;
-      cfg.numAttrs = c->pdl ? 2 : 1;
+      c->cur_kbit = 2;
+      cfg.numAttrs = pdl_for(c) ? 2 : 1;
       PROFILED(K_BWD, s, ([&]() -> whale_status_t {
                  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, c->tmG_dx, c->tmW_dx, c->tmDxPart, c->tmG_dw, c->tmX_dw,
                                              c->tmDW, b));
@@ -1381,7 +1395,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
         if (st != WHALE_OK) return st;
       }
       PROFILED(K_BWD, s,
-               (launch(c, kern, dim3(grid), dim3(kBwdThreads), c->bwd_smem, s, c->tmG_dx, c->tmW_dx, c->tmDxPart,
+               (c->cur_kbit = 2, launch(c, kern, dim3(grid), dim3(kBwdThreads), c->bwd_smem, s, c->tmG_dx, c->tmW_dx, c->tmDxPart,
                        c->tmG_dw, c->tmX_dw, c->tmDW, b)));
     }
   } else if constexpr (ES == 2) {
@@ -1440,7 +1454,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
         c->nvls_rs ? reinterpret_cast<const float4*>(c->mc + L.dxrecv + static_cast<size_t>(p.rank) * p.Bmax * p.D * 4)
                    : nullptr;
     PROFILED(K_RS_REDUCE, s,
-             (launch(c, dx_reduce_kernel<ES>, dim3(g2), dim3(256), 0, s,
+             (c->cur_kbit = 4, launch(c, dx_reduce_kernel<ES>, dim3(g2), dim3(256), 0, s,
                      reinterpret_cast<const float4*>(c->symm[p.rank] + L.dxrecv), static_cast<int>(p.B),
                      static_cast<int>(p.Bmax), static_cast<int>(p.D), p.world, my_flags, static_cast<const uint32_t*>(dev_epoch), dx_local,
                      err, mc_mine)));

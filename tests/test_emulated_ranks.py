@@ -248,3 +248,23 @@ def test_emulated_random_fuzz(whale):
         cap = [int(v) for v in rng.integers(1, 4, world)] if rng.integers(0, 2) else None
         run_emulated(whale, world, D=D, C=C, batch=batch, capacity=cap, regime=str(rng.choice(["init", "peaked"])),
                      bias=bool(rng.integers(0, 2)), steps=2, seed=3000 + case)
+
+
+@pytest.mark.parametrize("B,D,C", [(16, 512, 5000), (24, 192, 3001)])  # F1 and plain path
+def test_emulated_standalone_gather(whale, B, D, C, monkeypatch):
+    """WHALE_FUSED_GATHER=0: the bridge all-gather as its own kernel instead of the logits / F1
+    prologue (the default fuses it) -- same protocol, same results."""
+    monkeypatch.setenv("WHALE_FUSED_GATHER", "0")
+    run_emulated(whale, 2, D=D, C=C, B=B, regime="peaked", seed=77)
+
+
+def test_emulated_bwd_cta_pairs(whale):
+    """The fused backward as CTA pairs (cta_group::2) at N = 2: B_tot = 1024 x D = 4096 needs no
+    split-K, so the pairs run, and dX is pushed to the row owners from the paired fixup."""
+    ops, _ = whale.emulated_ranks(2001, 4096, 2, local_batch=512)
+    try:
+        assert all(o.config()["bwd_pair"] == 1 for o in ops), [o.config()["bwd_pair"] for o in ops]
+    finally:
+        for o in ops:
+            o.close()
+    run_emulated(whale, 2, D=4096, C=2001, B=512, regime="peaked", seed=78, steps=2)
