@@ -116,6 +116,9 @@ CASES = [
     (3, dict(batch=[30, 15, 15], D=512, C=9000)),
     (4, dict(batch=[40, 40, 40, 0], D=256, C=3000, regime="peaked")),
     (4, dict(batch=[12, 8, 8, 4], D=1024, C=12_011, regime="peaked", bias=True, expect_f1=True)),
+    # N = 8 (the largest world the library takes; gpurun boxes stop at 4 GPUs)
+    (8, dict(B=32, D=2048, C=20_000)),                            # c2-like rows per rank, plain path
+    (8, dict(B=4, D=512, C=20_000, regime="peaked", expect_f1=True)),  # F1 at N = 8 (B_tot = 32)
 ]
 
 
