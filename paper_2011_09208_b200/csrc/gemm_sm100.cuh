@@ -85,6 +85,11 @@ struct GemmArgs {
   // waits for the gathered A rows -- the W stream overlaps the NVLink exchange
   int gather_on;
   GatherArgs gather;
+  // EPI_FWD_STATS: P~ written straight from registers (each thread its row's 64-byte pieces)
+  // instead of through per-warp smem staging + TMA stores -- frees the 32 KB of staging for one
+  // more load stage when the whole batch is one M block (the N > 1 shard shapes)
+  void* p_direct;           // P~ base [M x ldp] (ES-sized elements) or NULL
+  long long p_ld;           // its row pitch in elements
   // step epoch: every kernel reads e = *dev_epoch + 1 (device-resident, so a whole step can
   // be captured once in a CUDA graph and replayed); the last backward kernel bumps it
   uint32_t* dev_epoch;
@@ -367,14 +372,17 @@ __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUte
     int am = 0x7fffffff;
     float zy = 0.f;
     bool has_zy = false;
+    const bool direct = a.p_direct != nullptr;
     if (wv) {
       for (int ch = g; ch < nch; ch += 2) {
-        if (lane == 0) {  // the store that last used this buffer has read it
-          if (nbw >= 4) bulk_wait_read<3>();
-          else if (nbw >= 2) bulk_wait_read<1>();
-          else bulk_wait_read<0>();
+        if (!direct) {
+          if (lane == 0) {  // the store that last used this buffer has read it
+            if (nbw >= 4) bulk_wait_read<3>();
+            else if (nbw >= 2) bulk_wait_read<1>();
+            else bulk_wait_read<0>();
+          }
+          __syncwarp();
         }
-        __syncwarp();
         uint8_t* b = ebuf + buf * kEpiBufBytes + lane * 128;
         for (int h = 0; h < kChunk; h += 32) {
           const int c0 = ch * kChunk + h;
@@ -426,6 +434,27 @@ __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUte
           }
           // this half-chunk's 16-byte pieces: bf16 -> 4 pieces at h / 8, fp32 -> 8 pieces
           constexpr int kPieces = 32 * ES / 16;
+          if (direct) {  // this row's 32 values straight to global (clipped to the valid columns)
+            if (rv) {
+              uint8_t* gp = static_cast<uint8_t*>(a.p_direct) +
+                            (static_cast<size_t>(row) * a.p_ld + static_cast<size_t>(bcol0 + c0)) * ES;
+              if (c0 + 32 <= ncol) {
+#pragma unroll
+                for (int k = 0; k < kPieces; ++k)
+                  *reinterpret_cast<uint4*>(gp + 16 * k) = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+              } else {
+                for (int c = 0; c < 32 && c0 + c < ncol; ++c) {
+                  if constexpr (ES == 2) {
+                    const uint32_t w2 = pk[c >> 1];
+                    *reinterpret_cast<uint16_t*>(gp + 2 * c) = static_cast<uint16_t>((c & 1) ? (w2 >> 16) : (w2 & 0xffffu));
+                  } else {
+                    *reinterpret_cast<uint32_t*>(gp + 4 * c) = pk[c];
+                  }
+                }
+              }
+            }
+            continue;
+          }
 #pragma unroll
           for (int k = 0; k < kPieces; ++k) {
             const int pc = (h * ES) / 16 + k;  // 16-byte piece within the 128-byte row
@@ -433,6 +462,7 @@ __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUte
                 make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
           }
         }
+        if (direct) continue;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {

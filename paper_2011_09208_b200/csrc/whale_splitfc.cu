@@ -161,6 +161,7 @@ struct GemmCfg {
   int stages = 0, stage_bytes = 0, epi_bufs = 2, smem = 0, grid = 0;
   int cluster = 1;  // 2: CTA pairs share (TMA-multicast) the B tile of M-adjacent tiles
   int a_rows = 128;  // K-major A rows per TMA box / smem stage (GemmArgs::a_rows)
+  bool p_direct = false;  // logits: P~ stored from registers, no epilogue staging (GemmArgs::p_direct)
 };
 
 static int env_int(const char* name, int dflt);
@@ -394,6 +395,17 @@ static whale_status_t build_plan(const whale_splitfc_desc* d, Plan& p, int sms) 
   };
   shrink_a(p.fwd, p.fwd.num_kb <= 4);  // as choose_plain
   shrink_a(p.dx, false);               // as choose_splitk
+  // logits with one M block (the N > 1 shard shapes): P~ from registers when dropping the 32 KB
+  // of epilogue staging buys another load stage (each CTA streams one or two long-K tiles)
+  if (p.fwd.m_blocks == 1 && p.fwd.cluster == 1 && env_int("WHALE_P_DIRECT", 1) != 0) {
+    const int stages0 = std::min(8, (kSmemLimit - kStaticSmemSlack - 1024 - 256) / p.fwd.stage_bytes);
+    if (stages0 > p.fwd.stages) {
+      p.fwd.p_direct = true;
+      p.fwd.epi_bufs = 0;
+      p.fwd.stages = stages0;
+      p.fwd.smem = gemm_smem_bytes(p.fwd.stages, p.fwd.stage_bytes, 0);
+    }
+  }
   {
     const char* e = getenv("WHALE_F1");
     p.f1 = p.es == 2 && p.Bt <= kF1NB && p.D % (kF1KC * 128) == 0 && p.D / kF1KC <= 1024 &&
@@ -1091,6 +1103,10 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
     a.s_tile = wsp<float>(c, L.s_tile);
     a.zy = wsp<float>(c, L.zy);
     a.err = err;
+    if (p.fwd.p_direct) {
+      a.p_direct = c->ws + L.P;
+      a.p_ld = static_cast<long long>(p.ldp);
+    }
     if (p.world > 1) {
       a.wait_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_GATHER * kMaxRanks;
       a.wait_count = p.world;
