@@ -287,6 +287,15 @@ __device__ __forceinline__ void end_of_step_ticket(const GemmArgs& a, uint32_t e
   }
 }
 
+// Debug timeline of the logits kernel (WHALE_EPI_DEBUG bit 16, results unaffected): per CTA
+// [entry, after prologue, producer's last load issued, MMA's last commit, epilogue's first
+// accumulator, epilogue done] in globaltimer ns -- whale_debug_gemm_timeline.
+__device__ unsigned long long g_gemm_cta[160 * 6];
+#define WHALE_GEMM_STAMP(slot)                                                              \
+  do {                                                                                     \
+    if ((a.debug & 16) && blockIdx.x < 160) g_gemm_cta[blockIdx.x * 6 + (slot)] = gtime_ns(); \
+  } while (0)
+
 // Split-FC forward epilogue (EPI_FWD_STATS) by warps 4..11: warp w reads TMEM lane quadrant
 // w % 4 (one thread per output row) and belongs to column group g = (w - 4) / 4, which owns the
 // tile's P~ chunks (128-byte rows: 128 / ES columns) g, g + 2, ...  Pass 1: row max over the
@@ -319,6 +328,7 @@ __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUte
     const int acc = it & 1;
     mbar_wait(&tfull[acc], (it >> 1) & 1);
     tc_fence_after();
+    if (it == 0 && threadIdx.x == 128) WHALE_GEMM_STAMP(4);
     const uint32_t tbase = tmem_base + acc * kMaxBN + (static_cast<uint32_t>(q * 32) << 16);
     const int row0 = mb * kBM + q * 32;
     const int row = row0 + lane;
@@ -491,6 +501,7 @@ __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUte
     }
   }
   if (lane == 0) bulk_wait<0>();
+  if (threadIdx.x == 128) WHALE_GEMM_STAMP(5);
 }
 
 // ES = operand element size: 2 -> bf16 (kind::f16), 4 -> fp32 storage run as kind::tf32.
@@ -513,6 +524,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
   uint64_t* tfull = empty + a.stages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  if (EPI == EPI_FWD_STATS && threadIdx.x == 0) WHALE_GEMM_STAMP(0);
 
   constexpr int kBK = kRowBytes / ES;        // K elements per stage
   constexpr int kAtom = kRowBytes / ES;      // MN elements per swizzle atom (MN-major)
@@ -554,6 +566,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
   pdl_trigger();
   TraceScope _trace(EPI == EPI_FWD_STATS ? 1 : (a.fix_mode != FIX_NONE ? 5 : 4));
   const uint32_t e = ld_acquire_gpu(a.dev_epoch) + 1u;  // this step's epoch
+  if (EPI == EPI_FWD_STATS && threadIdx.x == 0) WHALE_GEMM_STAMP(1);
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -651,6 +664,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
           }
         }
       }
+      if (EPI == EPI_FWD_STATS) WHALE_GEMM_STAMP(2);
       if (!a_ready) {  // fewer k-blocks than ring stages (or no tile)
         for (int p = 0; p < a.wait_count; ++p) wait_flag_geq(a.wait_flags + p, e * a.wait_mult, a.err, ERR_COMM | ERR_AT_GATHER);
         fence_proxy_async_global();
@@ -710,6 +724,7 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
         if constexpr (PAIR) umma_commit_pair_mc(&tfull[acc], 0x3);  // both halves ready
         else umma_commit(&tfull[acc]);                     // accumulator ready for the epilogue
       }
+      if (EPI == EPI_FWD_STATS) WHALE_GEMM_STAMP(3);
     }
   } else if (EPI == EPI_FWD_STATS && warp >= 4) {
     // ===================== logits epilogue: 8 warps, 2 column groups =====================

@@ -1655,6 +1655,13 @@ extern "C" int whale_debug_f1_max_clusters(int smem) {
   return n;
 }
 
+// Internal: read the logits debug timeline (160 CTAs x {entry, after prologue, last load issued,
+// last MMA commit, first accumulator in the epilogue, epilogue done}; WHALE_EPI_DEBUG=16).
+extern "C" int whale_debug_gemm_timeline(unsigned long long* out) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+  return cudaMemcpyFromSymbol(out, g_gemm_cta, sizeof(g_gemm_cta)) == cudaSuccess ? 0 : -2;
+}
+
 // Internal: read the backward debug timeline (160 CTAs x {start, dX unit done, epilogue done,
 // GEMM units}; WHALE_EPI_DEBUG=16).  Synchronises the device.
 extern "C" int whale_debug_bwd_timeline(unsigned long long* out) {

@@ -75,6 +75,17 @@ if os.environ.get("WHALE_F1_DBG"):  # F1 per-CTA [entry, after prologue, end] of
         if os.environ.get("F1_CTA_DUMP"):
             rel = lambda v: [round((x - t0) / 1e3, 2) for x in v]
             json.dump({"entry": rel(ent), "end": rel(en), "sync": rel(cs), "exit": rel(ex)}, open(os.environ["F1_CTA_DUMP"], "w"))
+if os.environ.get("GEMM_TL"):  # logits per-CTA timeline (needs WHALE_EPI_DEBUG=16)
+    L.whale_debug_gemm_timeline.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+    tg = (ctypes.c_ulonglong * 960)()
+    L.whale_debug_gemm_timeline(tg)
+    n = sum(1 for c in range(160) if tg[6 * c] and tg[6 * c + 5])
+    cols = [[tg[6 * c + k] for c in range(160) if tg[6 * c] and tg[6 * c + 5]] for k in range(6)]
+    g0 = min(cols[0])
+    q = lambda v: [round((x - g0) / 1e3, 1) for x in (min(v), sorted(v)[len(v) // 2], max(v))]
+    print(json.dumps({"rank": rank, "gemm_ctas": n, "entry": q(cols[0]), "after_prologue": q(cols[1]),
+                      "last_load_issued": q(cols[2]), "last_mma_commit": q(cols[3]), "first_acc": q(cols[4]),
+                      "epilogue_done": q(cols[5])}))
 if os.environ.get("BWD_TL"):  # backward per-CTA timeline (needs WHALE_EPI_DEBUG=16)
     L.whale_debug_bwd_timeline.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
     tb = (ctypes.c_ulonglong * 640)()
