@@ -75,6 +75,15 @@ struct BwdArgs {
   void* dw_ptr;         // dW_r [C_r x D] fp32 or bf16 (row-bulk stores)
   int dw_ld;            // D
   int dw_bf16;          // 1: dW_r is stored in bf16 (RN-even from the fp32 accumulator)
+  // N > 1: the owner side of the dX reduce-scatter in this kernel's tail (instead of the
+  // dx_reduce kernel): after the end-of-step ticket every CTA waits for all ranks' RS flags
+  // and sums its slice of this rank's rows over the N receive slots in rank order
+  int red_on;
+  const float4* red_recv;    // this rank's receive slab [world][Bslab x D] fp32
+  const float4* red_mc;      // NVLS: slot `rank` of every rank's slab (multicast view) or NULL
+  const uint32_t* red_flags; // &flag[RS][0] on this rank
+  void* red_out;             // dX_r bf16 [B x D]
+  int red_B, red_Bslab;
 };
 
 constexpr int kBwdThreads = 384;  // 12 warps (8..11: G-fused operand transformers)
@@ -709,6 +718,30 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     else tmem_dealloc(tmem_base, kTmemCols);
   }
   end_of_step_ticket(a.dx, e, s_fix_go, a.sched_cnt, /*pushes_fenced=*/true);  // RS flags (N > 1) + epoch publish + counter reset
+  if (a.red_on) {  // A8 owner side (as dx_reduce_kernel): every rank's pushes for my rows have landed
+    if (threadIdx.x < a.dx.world) wait_flag_geq(a.red_flags + threadIdx.x, e, a.dx.err, ERR_COMM | ERR_AT_RS);
+    __syncthreads();
+    __threadfence_system();
+    const int64_t total = static_cast<int64_t>(a.red_B) * (a.dx.N / 4);
+    const int64_t slab = static_cast<int64_t>(a.red_Bslab) * (a.dx.N / 4);
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+      float4 acc;
+      if (a.red_mc != nullptr) {
+        acc = multimem_ld_reduce_add_v4f32(a.red_mc + i);
+      } else {
+        acc = __ldcg(a.red_recv + i);
+        for (int p = 1; p < a.dx.world; ++p) {
+          const float4 v = __ldcg(a.red_recv + p * slab + i);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      }
+      uint2 o;
+      o.x = pack_bf16x2(acc.x, acc.y);
+      o.y = pack_bf16x2(acc.z, acc.w);
+      reinterpret_cast<uint2*>(a.red_out)[i] = o;
+    }
+  }
 }
 
 }  // namespace whale

@@ -584,6 +584,7 @@ struct whale_splitfc_ctx {
   bool fused_gather = true;          // N > 1: bridge all-gather inside the logits / F1 prologue
   bool bwd_pair = false;             // fused backward as CTA pairs (cta_group::2)
   bool nvls_rs = false;              // dX reduce-scatter through the NVSwitch (multimem.ld_reduce)
+  bool fused_reduce = true;          // N > 1: the owner reduce in the fused backward's tail
   bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
@@ -830,6 +831,7 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
   }
   c->fused_bwd = p.es == 2 && env_int("WHALE_FUSED_BWD", 1) != 0 && g_store_mode == 1;
   c->fused_gather = env_int("WHALE_FUSED_GATHER", 1) != 0;
+  c->fused_reduce = env_int("WHALE_FUSED_REDUCE", 1) != 0;
   c->gfuse = c->fused_bwd && env_int("WHALE_GFUSE", 0) != 0;
   if (p.dw_bf16 && !c->fused_bwd) {
     delete c;
@@ -1374,6 +1376,16 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     b.stage_bytes = c->bwd_stage_bytes;
     b.epi_bufs = c->bwd_epi_bufs;
     b.sched_cnt = counters + CNT_SCHED;
+    if (p.world > 1 && c->fused_reduce) {  // A8 owner side in the backward's tail
+      b.red_on = 1;
+      b.red_recv = reinterpret_cast<const float4*>(c->symm[p.rank] + L.dxrecv);
+      b.red_mc = c->nvls_rs ? reinterpret_cast<const float4*>(c->mc + L.dxrecv + static_cast<size_t>(p.rank) * p.Bmax * p.D * 4)
+                            : nullptr;
+      b.red_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_RS * kMaxRanks;
+      b.red_out = dx_local;
+      b.red_B = static_cast<int>(p.B);
+      b.red_Bslab = static_cast<int>(p.Bmax);
+    }
     if (c->bwd_pair) {  // CTA pairs: units are pair tiles, the grid is 2-CTA clusters
       b.ux = p.dx.num_tiles / 2;
       b.tw = p.dw.num_tiles / 2;
@@ -1459,8 +1471,8 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     PROFILED(K_DX, s,
              (launch_gemm<EPI_STORE_F32, false, false, 4>(c, 5, p.dx, c->tmG_dx, c->tmWT, c->tmDxPart, ax, s)));
   }
-  // ---- A8 owner side of the reduce-scatter (N > 1)
-  if (p.world > 1) {
+  // ---- A8 owner side of the reduce-scatter (N > 1), unless the fused backward did it
+  if (p.world > 1 && !(ES == 2 && c->fused_bwd && c->fused_reduce)) {
     const int64_t own = p.B * p.D / 4;
     const int g2 = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(cdiv(own, 256), c->shared_device ? std::max(1, p.sms / 8) : 2 * p.sms)));
@@ -1525,6 +1537,7 @@ extern "C" int32_t whale_splitfc_launches_per_step(const whale_splitfc_ctx* ctx)
   int base = ctx->p.world == 1 ? 4 : 6;
   if (ctx->fused_bwd) base -= 1;  // dW + dX share one launch (F1: dW tiles + dX combine units)
   if (ctx->p.world > 1 && ctx->fused_gather) base -= 1;  // the gather runs in the logits / F1 prologue
+  if (ctx->p.world > 1 && ctx->fused_bwd && ctx->fused_reduce && ctx->p.es == 2) base -= 1;  // owner reduce in the backward
   // F1 unfused: the combine kernel replaces the dX GEMM (same count)
   return base + (ctx->p.es == 4 ? 3 : 0);  // fp32 path: operand transposes
 }
