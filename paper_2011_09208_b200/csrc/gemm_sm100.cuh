@@ -453,7 +453,9 @@ __device__ __forceinline__ void fwd_stats_epilogue(const GemmArgs& a, const CUte
                 for (int k = 0; k < kPieces; ++k)
                   *reinterpret_cast<uint4*>(gp + 16 * k) = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
               } else {
-                for (int c = 0; c < 32 && c0 + c < ncol; ++c) {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {  // unrolled: pk stays in registers (static indices)
+                  if (c0 + c >= ncol) continue;
                   if constexpr (ES == 2) {
                     const uint32_t w2 = pk[c >> 1];
                     *reinterpret_cast<uint16_t*>(gp + 2 * c) = static_cast<uint16_t>((c & 1) ? (w2 >> 16) : (w2 & 0xffffu));
