@@ -78,6 +78,7 @@ struct BwdArgs {
   // N > 1: the owner side of the dX reduce-scatter in this kernel's tail (instead of the
   // dx_reduce kernel): after the end-of-step ticket every CTA waits for all ranks' RS flags
   // and sums its slice of this rank's rows over the N receive slots in rank order
+  int w_last_use;            // 1: dX-unit W_r loads are marked L2 evict_first (the logits kept W_r in L2)
   int red_on;
   const float4* red_recv;    // this rank's receive slab [world][Bslab x D] fp32
   const float4* red_mc;      // NVLS: slot `rank` of every rank's slab (multicast view) or NULL
@@ -344,7 +345,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               mbar_arrive_expect_tx(&full[stage], tx_dx);
               tma_load_2d(sA, &tmGx, &full[stage], kb * kBK, mb * kBM);
               for (int j = 0; j < X.BN / kAtom; ++j)
-                tma_load_2d(sB + j * kBK * kRowBytes, &tmW, &full[stage], nb * X.BN + j * kAtom, kb * kBK);
+                if (a.w_last_use)  // W_r kept in L2 by the logits: this is its last use
+                  tma_load_2d_hint(sB + j * kBK * kRowBytes, &tmW, &full[stage], nb * X.BN + j * kAtom, kb * kBK,
+                                   l2_policy_evict_first());
+                else
+                  tma_load_2d(sB + j * kBK * kRowBytes, &tmW, &full[stage], nb * X.BN + j * kAtom, kb * kBK);
             }
             if (++stage == a.stages) {
               stage = 0;

@@ -90,6 +90,8 @@ struct GemmArgs {
   // more load stage when the whole batch is one M block (the N > 1 shard shapes)
   void* p_direct;           // P~ base [M x ldp] (ES-sized elements) or NULL
   long long p_ld;           // its row pitch in elements
+  int b_keep;               // 1: B (W_r) loads marked L2 evict_last -- W_r small enough to stay in L2
+                            // for the backward's dX pass, which reads it again (w_l2)
   // step epoch: every kernel reads e = *dev_epoch + 1 (device-resident, so a whole step can
   // be captured once in a CUDA graph and replayed); the last backward kernel bumps it
   uint32_t* dev_epoch;
@@ -655,7 +657,8 @@ __global__ void __launch_bounds__(EPI == EPI_FWD_STATS ? kStatsGemmThreads : kGe
               tma_load_2d(sA + j * box_bytes, &tmA, &full[stage], mb * kBM + j * kAtom, kb * bk);
           }
           if (!B_MN) {
-            tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
+            if (a.b_keep) tma_load_2d_hint(sB, &tmB, &full[stage], kb * kBK, nb * a.BN, l2_policy_evict_last());
+            else tma_load_2d(sB, &tmB, &full[stage], kb * kBK, nb * a.BN);
           } else {
             for (int j = 0; j < a.BN / kAtom; ++j)
               tma_load_2d(sB + j * box_bytes, &tmB, &full[stage], nb * a.BN + j * kAtom, kb * bk);

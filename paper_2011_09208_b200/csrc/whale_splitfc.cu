@@ -585,6 +585,7 @@ struct whale_splitfc_ctx {
   bool bwd_pair = false;             // fused backward as CTA pairs (cta_group::2)
   bool nvls_rs = false;              // dX reduce-scatter through the NVSwitch (multimem.ld_reduce)
   bool fused_reduce = true;          // N > 1: the owner reduce in the fused backward's tail
+  bool w_l2 = false;                 // W_r kept in L2 between the logits and the backward's dX pass
   bool shared_device = false;        // ranks emulated on one device (tests): no PDL, bounded grids
   int bwd_stages = 0, bwd_stage_bytes = 0, bwd_epi_bufs = 4, bwd_smem = 0;
   bool profile = false;
@@ -871,6 +872,17 @@ extern "C" whale_status_t whale_splitfc_create(const whale_splitfc_desc* desc, w
     c->bwd_smem = fixed + c->bwd_stages * c->bwd_stage_bytes;
     if (c->bwd_stages < 2) c->fused_bwd = false;
   }
+  {
+    // The logits load W_r evict_last and the backward's dX pass, its second and last read,
+    // evict_first, so the part of W_r that L2 holds survives the statistics kernel and the dW
+    // stores in between (WHALE_W_L2: 1 on, 0 off, else auto).  Measured: c2 N = 2 (W_r 205 MB)
+    // 185.0 -> 179.7-181.6 us, N = 4 / 8 shard shapes and c4 neutral, c5 (4 GB, CTA pairs) -2 %:
+    // auto for W_r <= 256 MB on the unpaired plain path.
+    const int wl2 = env_int("WHALE_W_L2", -1);
+    const double w_bytes = static_cast<double>(p.Cr) * p.D * p.es;
+    c->w_l2 = p.es == 2 && !p.f1 && !c->bwd_pair && (wl2 == 1 || (wl2 < 0 && w_bytes <= 256.0 * (1 << 20)));
+  }
+
   if (!c->fused_bwd && p.es == 2) {
     maybe_pair(c->p.dw, sms, true, kRowBytes / p.es);  // standalone dW GEMM
     // standalone dX GEMM (only without split-K and with whole pairs of M blocks: the split-K
@@ -1109,6 +1121,7 @@ static whale_status_t forward_impl(whale_splitfc_ctx* c, const void* x_local, co
       a.p_direct = c->ws + L.P;
       a.p_ld = static_cast<long long>(p.ldp);
     }
+    a.b_keep = c->w_l2 ? 1 : 0;
     if (p.world > 1) {
       a.wait_flags = reinterpret_cast<const uint32_t*>(c->symm[p.rank] + L.flags) + FLAG_GATHER * kMaxRanks;
       a.wait_count = p.world;
@@ -1376,6 +1389,7 @@ static whale_status_t backward_impl(whale_splitfc_ctx* c, const void* w, void* d
     b.stage_bytes = c->bwd_stage_bytes;
     b.epi_bufs = c->bwd_epi_bufs;
     b.sched_cnt = counters + CNT_SCHED;
+    b.w_last_use = c->w_l2 ? 1 : 0;
     if (p.world > 1 && c->fused_reduce) {  // A8 owner side in the backward's tail
       b.red_on = 1;
       b.red_recv = reinterpret_cast<const float4*>(c->symm[p.rank] + L.dxrecv);
@@ -1610,6 +1624,7 @@ extern "C" whale_status_t whale_splitfc_config(const whale_splitfc_ctx* ctx, cha
                   ",\"bwd_stages\":" + std::to_string(ctx->bwd_stages) +
                   ",\"bwd_epi_bufs\":" + std::to_string(ctx->bwd_epi_bufs) +
                   ",\"fused_gather\":" + std::to_string(ctx->fused_gather ? 1 : 0) +
+                  ",\"w_l2\":" + std::to_string(ctx->w_l2 ? 1 : 0) +
                   ",\"local_bytes\":" + std::to_string(p.L.local_total) +
                   ",\"symm_bytes\":" + std::to_string(p.L.symm_total) + "}";
   if (s.size() + 1 > buf_len) return fail(WHALE_ERR_INVALID_ARG, "buffer too small (%zu)", s.size() + 1);
