@@ -17,6 +17,13 @@ if world > 1:
 rank = int(os.environ.get("RANK", "0"))
 local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local); dev = torch.device("cuda", local)
+if os.environ.get("PERSIST_MB"):  # experiment: L2 set-aside for persisting (evict_last) lines
+    torch.zeros(1, device=dev)
+    rt = ctypes.CDLL("/usr/local/cuda/lib64/libcudart.so.12")
+    rc = rt.cudaDeviceSetLimit(ctypes.c_int(0x06), ctypes.c_size_t(int(os.environ["PERSIST_MB"]) << 20))
+    got = ctypes.c_size_t(0)
+    rt.cudaDeviceGetLimit(ctypes.byref(got), ctypes.c_int(0x06))
+    print(json.dumps({"persisting_l2_set_rc": rc, "persisting_l2_bytes": got.value}))
 cfg = syn.CONFIGS[os.environ.get("CFG", "c2")]
 if os.environ.get("B") or os.environ.get("C"):  # shape overrides (e.g. one rank's shard shape at N = 1)
     import dataclasses
