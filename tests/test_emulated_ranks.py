@@ -271,3 +271,45 @@ def test_emulated_bwd_cta_pairs(whale):
         for o in ops:
             o.close()
     run_emulated(whale, 2, D=4096, C=2001, B=512, regime="peaked", seed=78, steps=2)
+
+
+def _one_step(whale, world, B, D, C, seed):
+    ops, streams = whale.emulated_ranks(C, D, world, local_batch=B)
+    dev = ops[0].device
+    try:
+        W = syn.gen_weight((0, C), D, seed, "peaked", "bf16")
+        X = syn.gen_features((0, world * B), D, seed + 1, "bf16")
+        y = syn.gen_labels((0, world * B), C, seed + 1)
+        keep, outs = [], []
+        for r, o in enumerate(ops):
+            with torch.cuda.stream(streams[r]):
+                xr, yr = X[r * B:(r + 1) * B].to(dev), y[r * B:(r + 1) * B].to(dev)
+                wr = W[o.o_r:o.o_r + o.C_r].to(dev).contiguous()
+                keep.append((xr, yr, wr))
+                o.forward(xr, yr, wr, row_loss=True)
+        for r, o in enumerate(ops):
+            with torch.cuda.stream(streams[r]):
+                outs.append(o.backward(keep[r][2]))
+        torch.cuda.synchronize(dev)
+        res = []
+        for r, o in enumerate(ops):
+            o.check()
+            res.append((o.loss.clone().cpu(), o.row_loss.clone().cpu(), outs[r][0].clone().cpu(), outs[r][1].clone().cpu()))
+        return res
+    finally:
+        for o in ops:
+            o.close()
+
+
+@pytest.mark.parametrize("knob", ["WHALE_FUSED_GATHER", "WHALE_FUSED_REDUCE", "WHALE_W_L2", "WHALE_SHRINK_A",
+                                  "WHALE_P_DIRECT"])
+@pytest.mark.parametrize("B,D,C", [(32, 512, 6001), (16, 512, 5000)])  # plain path (B_tot = 64) and F1
+def test_emulated_fusions_bitwise(whale, knob, B, D, C, monkeypatch):
+    """The round-2 fusions and placement choices change where the work runs, not the arithmetic:
+    with each switched off the loss, per-row loss, dX and dW of every rank are bit-identical."""
+    on = _one_step(whale, 2, B, D, C, 31)
+    monkeypatch.setenv(knob, "0")
+    off = _one_step(whale, 2, B, D, C, 31)
+    for r in range(2):
+        for a, b in zip(on[r], off[r]):
+            assert torch.equal(a, b), (knob, r)
