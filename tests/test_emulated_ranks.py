@@ -119,6 +119,7 @@ CASES = [
     # N = 8 (the largest world the library takes; gpurun boxes stop at 4 GPUs)
     (8, dict(B=32, D=2048, C=20_000)),                            # c2-like rows per rank, plain path
     (8, dict(B=4, D=512, C=20_000, regime="peaked", expect_f1=True)),  # F1 at N = 8 (B_tot = 32)
+    (8, dict(B=32, D=1024, C=20_001, capacity=[2, 1, 1, 1, 1, 1, 1, 1])),  # c3's 2:1:...:1 plan on 8 ranks
 ]
 
 
